@@ -1,0 +1,206 @@
+"""ORACLE — test infrastructure only.
+
+A plain, slow, obviously-correct CPU FP64 implementation of what the hot path of
+arXiv 2311.11833 computes (Alg. 1):
+
+  1. perturb A by +/- alpha*eps*D for each lane (Eqs. (5)-(6));
+  2. pivot-free ("static pivoting") LU + forward/back substitution per lane
+     (oracle.c: dense OR1, and sparse OR2 for sizes where O(n^3) is infeasible);
+  3-4. combine the lanes with the weights of Remark 2 / Eq. (13) (weights.py,
+     exact rationals; oracle.c: oracle_combine);
+  5. optional error test: residual ||A x - b|| and the partial-pivot x* (oracle.c).
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+reference leg may import this package.  It shares no code with the CUDA path
+(paper_2311_11833_b200/) and never imports it; it takes its inputs only from
+psp_inputs/ (seeded generators, no method arithmetic).
+
+Parity pins: see tests/test_oracle_*.py (every function here is pinned; none is
+"parity unpinned").
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+from . import ordering, weights  # noqa: F401
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c (gcc, -O2, -ffp-contract=off, OpenMP over lanes)."""
+    src = os.path.join(_HERE, "oracle.c")
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(src):
+        tmp = _LIB_PATH + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math",
+                               "-fopenmp", "-fPIC", "-shared", "-o", tmp, src, "-lm"])
+        os.replace(tmp, _LIB_PATH)
+    return _LIB_PATH
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB_PATH)
+        P, I, D = ctypes.c_void_p, ctypes.c_int, ctypes.c_double
+        L.oracle_lu_nopivot.argtypes = [I, P, D]
+        L.oracle_lu_solve.argtypes = [I, P, P]
+        L.oracle_lu_partial_pivot.argtypes = [I, P, P]
+        L.oracle_lu_pp_solve.argtypes = [I, P, P, P]
+        L.oracle_dense_lane.argtypes = [I, P, P, P, P, P, D, I, P, D, P]
+        L.oracle_dense_batch.argtypes = [I, P, P, P, P, P, I, P, I, P, D, P, P]
+        L.oracle_dense_batch.restype = None
+        L.oracle_reference_solve.argtypes = [I, P, P, P, I, P, P]
+        L.oracle_sparse_lu.argtypes = [I, P, P, P, P, P, P, D, D, P]
+        L.oracle_sparse_solve.argtypes = [I, P, P, P, P, P, P]
+        L.oracle_sparse_batch.argtypes = [I, P, P, P, P, P, P, P, I, P, I, P, D, P, P]
+        L.oracle_sparse_batch.restype = None
+        L.oracle_combine.argtypes = [I, I, I, I, P, P, P]
+        L.oracle_combine.restype = None
+        L.oracle_num_threads.restype = I
+        L.oracle_set_num_threads.argtypes = [I]
+        _lib = L
+    return _lib
+
+
+def _p(a):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _c(a, dt):
+    return np.ascontiguousarray(a, dtype=dt)
+
+
+def num_threads() -> int:
+    return lib().oracle_num_threads()
+
+
+def set_num_threads(t: int) -> None:
+    lib().oracle_set_num_threads(int(t))
+
+
+def lu_nopivot(A, tol=0.0):
+    """Dense pivot-free LU of a copy of A -> (LU, status)."""
+    LU = _c(A, np.float64).copy()
+    st = lib().oracle_lu_nopivot(LU.shape[0], _p(LU), float(tol))
+    return LU, st
+
+
+def lu_solve(LU, b):
+    y = _c(b, np.float64).copy()
+    lib().oracle_lu_solve(LU.shape[0], _p(_c(LU, np.float64)), _p(y))
+    return y
+
+
+def lu_partial_pivot(A):
+    LU = _c(A, np.float64).copy()
+    piv = np.zeros(LU.shape[0], dtype=np.int32)
+    st = lib().oracle_lu_partial_pivot(LU.shape[0], _p(LU), _p(piv))
+    return LU, piv, st
+
+
+def lu_pp_solve(LU, piv, b):
+    y = _c(b, np.float64).copy()
+    lib().oracle_lu_pp_solve(LU.shape[0], _p(_c(LU, np.float64)), _p(_c(piv, np.int32)), _p(y))
+    return y
+
+
+def default_tol(n, row_ptr, col_idx, vals):
+    """zero_tol = n * u * ||A||_1 of the unperturbed A (reading R10)."""
+    cs = np.zeros(n)
+    np.add.at(cs, np.asarray(col_idx), np.abs(np.asarray(vals)))
+    return n * np.finfo(np.float64).eps * float(cs.max())
+
+
+def dense_batch(sysm, perm, eps, tol, B=None):
+    """OR1 over all lanes: returns X [K, R, n] (original ordering) and status [K]."""
+    n = sysm.n
+    eps = _c(eps, np.float64)
+    B = sysm.b if B is None else B
+    R = B.shape[1]
+    Bc = _c(B.T, np.float64)  # R x n contiguous == n x R column-major
+    X = np.empty((len(eps), R, n))
+    st = np.zeros(len(eps), dtype=np.int32)
+    lib().oracle_dense_batch(n, _p(_c(sysm.row_ptr, np.int32)), _p(_c(sysm.col_idx, np.int32)),
+                             _p(_c(sysm.vals, np.float64)), _p(_c(perm, np.int32)),
+                             _p(_c(sysm.d, np.float64)), len(eps), _p(eps), R, _p(Bc),
+                             float(tol), _p(X), _p(st))
+    return X, st
+
+
+class SparseOracle:
+    """OR2: the oracle's own symbolic (ordering.filled_pattern) + sparse numeric."""
+
+    def __init__(self, sysm, perm):
+        n = sysm.n
+        self.n, self.perm = n, _c(perm, np.int32)
+        self.fcp, self.fri = ordering.filled_pattern(n, sysm.row_ptr, sysm.col_idx, perm)
+        self.acp, self.ari, self.av = ordering.permuted_csc(n, sysm.row_ptr, sysm.col_idx,
+                                                            sysm.vals, perm)
+        self.dp = _c(np.asarray(sysm.d)[self.perm], np.float64)
+        self.b = sysm.b
+
+    @property
+    def nnz_lu(self):
+        return int(self.fcp[-1])
+
+    def batch(self, eps, tol, B=None):
+        eps = _c(eps, np.float64)
+        B = self.b if B is None else B
+        R = B.shape[1]
+        Bc = _c(B.T, np.float64)
+        X = np.empty((len(eps), R, self.n))
+        st = np.zeros(len(eps), dtype=np.int32)
+        lib().oracle_sparse_batch(self.n, _p(self.acp), _p(self.ari), _p(self.av), _p(self.fcp),
+                                  _p(self.fri), _p(self.dp), _p(self.perm), len(eps), _p(eps), R,
+                                  _p(Bc), float(tol), _p(X), _p(st))
+        return X, st
+
+    def factor(self, eps, tol):
+        fv = np.empty(max(self.nnz_lu, 1))
+        st = lib().oracle_sparse_lu(self.n, _p(self.acp), _p(self.ari), _p(self.av), _p(self.fcp),
+                                    _p(self.fri), _p(self.dp), float(eps), float(tol), _p(fv))
+        return fv, st
+
+
+def reference_solve(sysm, B=None):
+    """x* = A^{-1} b by partial-pivot GE (the unperturbed system)."""
+    B = sysm.b if B is None else B
+    R = B.shape[1]
+    Bc = _c(B.T, np.float64)
+    X = np.empty((R, sysm.n))
+    st = lib().oracle_reference_solve(sysm.n, _p(_c(sysm.row_ptr, np.int32)),
+                                      _p(_c(sysm.col_idx, np.int32)), _p(_c(sysm.vals, np.float64)),
+                                      R, _p(Bc), _p(X))
+    return X, st
+
+
+def combine(weights_WK, X):
+    """x_hat[w] = sum_k W[w,k] x_k (ascending k, fma) -> [W, R, n]."""
+    Wm = _c(weights_WK, np.float64)
+    X = _c(X, np.float64)
+    K, R, n = X.shape
+    out = np.empty((Wm.shape[0], R, n))
+    lib().oracle_combine(K, R, n, Wm.shape[0], _p(Wm), _p(X), _p(out))
+    return out
+
+
+def ladder_weight_matrix(ladders):
+    """W x K dense weights for a list of ladders laid out consecutively in lane
+    order (ladder g occupies lanes [2*sum_{h<g} m_h, ...)); one recovered solution
+    per ladder, weights beta_j/2 per sign (weights.lane_weights)."""
+    K = 2 * sum(len(l) for l in ladders)
+    Wm = np.zeros((len(ladders), K))
+    k0 = 0
+    for g, mags in enumerate(ladders):
+        lw = weights.lane_weights(mags)
+        Wm[g, k0:k0 + len(lw)] = lw
+        k0 += len(lw)
+    return Wm

@@ -1,0 +1,119 @@
+"""ORACLE (test infrastructure only): elimination order and filled pattern.
+
+The paper eliminates in the natural order of a dense matrix (getrf).  A
+sparse solver must choose an elimination order; the result x_k of each lane is
+independent of it in exact arithmetic, but its rounding is not, so for
+element-by-element parity the oracle eliminates in the same order as the CUDA
+path.  It does NOT take that order from the product: it computes it itself, with
+the textbook exact minimum-degree rule (reading R13):
+
+  on the elimination graph of pattern(A + A^T) (self loops removed), repeatedly
+  eliminate the vertex of smallest current degree, ties to the smallest original
+  index; eliminating v joins its remaining neighbours into a clique and removes v.
+
+`first` (optional) forces one vertex to be eliminated first, then the rule
+continues on the rest — the 'leading-zero' stress convention ("A leading 0
+was always encountered on a diagonal").  The permutation is perm[new] = old.
+
+Parity of the permutation itself (integer, bit-exact) is checked against the
+product's in the GPU-free tests.
+"""
+from __future__ import annotations
+
+import heapq
+
+import numpy as np
+
+
+def symmetric_adjacency(n, row_ptr, col_idx):
+    adj = [set() for _ in range(n)]
+    for i in range(n):
+        for q in range(int(row_ptr[i]), int(row_ptr[i + 1])):
+            j = int(col_idx[q])
+            if j != i:
+                adj[i].add(j)
+                adj[j].add(i)
+    return adj
+
+
+def _eliminate(adj, v):
+    nb = adj[v]
+    for a in nb:
+        adj[a].discard(v)
+    nbl = list(nb)
+    for x in range(len(nbl)):
+        ax = adj[nbl[x]]
+        for y in range(len(nbl)):
+            if x != y:
+                ax.add(nbl[y])
+    adj[v] = set()
+    return nbl
+
+
+def min_degree_order(n, row_ptr, col_idx, first=None):
+    adj = symmetric_adjacency(n, row_ptr, col_idx)
+    alive = [True] * n
+    heap = [(len(adj[v]), v) for v in range(n)]
+    heapq.heapify(heap)
+    perm = []
+
+    def elim(v):
+        alive[v] = False
+        perm.append(v)
+        for a in _eliminate(adj, v):
+            heapq.heappush(heap, (len(adj[a]), a))
+
+    if first is not None:
+        elim(int(first))
+    while heap:
+        deg, v = heapq.heappop(heap)
+        if not alive[v] or deg != len(adj[v]):
+            continue
+        elim(v)
+    assert len(perm) == n
+    return np.array(perm, dtype=np.int32)
+
+
+def filled_pattern(n, row_ptr, col_idx, perm):
+    """Filled pattern of L+U for the symmetric-pattern elimination of P A P^T
+    (pattern(A+A^T) plus the diagonal, plus every fill edge the elimination graph
+    creates).  Returns CSC (colptr, rowind) in the permuted numbering, rows sorted."""
+    inv = np.empty(n, dtype=np.int64)
+    inv[np.asarray(perm)] = np.arange(n)
+    adj0 = symmetric_adjacency(n, row_ptr, col_idx)
+    adj = [set(int(inv[j]) for j in adj0[int(perm[i])]) for i in range(n)]
+    cols = [set([j]) for j in range(n)]
+    for p in range(n):
+        higher = sorted(a for a in adj[p] if a > p)
+        for i in higher:          # (i, p) in L and (p, i) in U
+            cols[p].add(i)
+            cols[i].add(p)
+        for x in higher:
+            for y in higher:
+                if x != y:
+                    adj[x].add(y)
+    colptr = np.zeros(n + 1, dtype=np.int32)
+    rows = []
+    for j in range(n):
+        r = sorted(cols[j])
+        rows += r
+        colptr[j + 1] = colptr[j] + len(r)
+    return colptr, np.array(rows, dtype=np.int32)
+
+
+def permuted_csc(n, row_ptr, col_idx, vals, perm):
+    """CSC of P A P^T (values copied, no arithmetic)."""
+    inv = np.empty(n, dtype=np.int64)
+    inv[np.asarray(perm)] = np.arange(n)
+    cols = [[] for _ in range(n)]
+    for i in range(n):
+        for q in range(int(row_ptr[i]), int(row_ptr[i + 1])):
+            cols[int(inv[col_idx[q]])].append((int(inv[i]), float(vals[q])))
+    colptr = np.zeros(n + 1, dtype=np.int32)
+    rows, vs = [], []
+    for j in range(n):
+        c = sorted(cols[j])
+        rows += [r for r, _ in c]
+        vs += [v for _, v in c]
+        colptr[j + 1] = colptr[j] + len(c)
+    return colptr, np.array(rows, dtype=np.int32), np.array(vs, dtype=np.float64)

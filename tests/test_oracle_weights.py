@@ -1,0 +1,79 @@
+"""Pins for oracle/weights.py (Remark 2 / Eq. (13))."""
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+from oracle import weights
+from golden_util import golden_rows
+
+
+def test_beta_m2_paper_example3():
+    # PAPER Example 3: beta = (1/3)[4, -1]
+    want = [Fraction(x) for x in golden_rows("paper_example3_beta_m2.txt")[0]]
+    assert weights.beta_integer(2) == want
+
+
+def test_gamma3_paper_eq12():
+    want = [[Fraction(x) for x in r] for r in golden_rows("paper_gamma3.txt")]
+    assert weights.gamma_matrix([1, 2, 3]) == want
+
+
+def test_beta_m3_derived():
+    # SPEC S:L328 [DERIVED]: m=3 -> [3/2, -3/5, 1/10]
+    assert weights.beta_integer(3) == [Fraction(3, 2), Fraction(-3, 5), Fraction(1, 10)]
+
+
+def test_beta_m1_trivial():
+    assert weights.beta_integer(1) == [Fraction(1)]
+
+
+@pytest.mark.parametrize("m", range(1, 16))
+def test_two_routes_agree(m):
+    # Vandermonde solve (paper's definition) == Lagrange basis at 0 (closed form)
+    assert weights.beta_vandermonde(list(range(1, m + 1))) == weights.beta_lagrange(list(range(1, m + 1)))
+
+
+@pytest.mark.parametrize("m", range(1, 7))
+def test_gamma_conditions(m):
+    # Eq. (17): gamma_0 = 1, gamma_2 = ... = gamma_{2(m-1)} = 0
+    beta = weights.beta_integer(m)
+    for k in range(m):
+        g = sum(b * Fraction(j + 1) ** (2 * k) for j, b in enumerate(beta))
+        assert g == (1 if k == 0 else 0)
+
+
+@pytest.mark.parametrize("m", range(1, 7))
+def test_beta_vs_lapack(m):
+    # library routine on the same Eq. (16) system, in floating point
+    G = np.array([[float((j + 1) ** (2 * i)) for j in range(m)] for i in range(m)])  # Gamma_m^T
+    e1 = np.zeros(m)
+    e1[0] = 1
+    ref = np.linalg.solve(G, e1)
+    got = np.array([float(b) for b in weights.beta_integer(m)])
+    assert np.allclose(got, ref, rtol=1e-9, atol=1e-12)
+
+
+def test_error_constants_paper():
+    for m, power, coef, sign_pinned in golden_rows("paper_error_constants.txt"):
+        m, power, coef, sign_pinned = int(m), int(power), int(coef), int(sign_pinned)
+        beta = weights.beta_integer(m)
+        # x_hat* = sum_k (sum_j beta_j j^{2k}) (A^{-1} eps D)^{2k} A^{-1} b  (Eq. (avg_hats))
+        got = sum(b * Fraction(j + 1) ** power for j, b in enumerate(beta))
+        if sign_pinned:
+            assert got == coef
+        else:
+            assert abs(got) == abs(coef)
+
+
+def test_geometric_ladder_weights_depend_on_ratios_only():
+    # beta depends only on node ratios: s = {1e-2, 5e-3} (ratio 1/2, cfg0) must give the
+    # integer-ladder m=2 weights with the order reversed (largest magnitude first).
+    got = weights.beta_lagrange([Fraction(2), Fraction(1)])
+    assert got == [Fraction(-1, 3), Fraction(4, 3)]
+
+
+def test_lane_weights_layout():
+    lw = weights.lane_weights([1.0, 2.0])
+    assert lw == [2 / 3, 2 / 3, -1 / 6, -1 / 6]
+    assert abs(sum(lw) - 1.0) < 1e-15
