@@ -1,0 +1,338 @@
+#!/usr/bin/env python
+"""Benchmark of the batched perturbation-induced static-pivoting hot path on B200.
+
+One STEP = one pass of the whole hot path (SURVEY §8(a) rows a1-a5, a6 when the
+recovered sums are split across ranks) over one batch: perturb + pivot-free LU of K
+lanes (psp_factor_batch), forward/back substitution (psp_solve_batch) and the
+weighted recombination (psp_recover).  Symbolic analysis (row a0) is done once per
+pattern, outside the timed region, and reported separately.
+
+Workload (N=1 line): the BASELINE configs[1] system — the synthetic 300-bus
+distributed-slack Jacobian, n = 531 — solved as a large batch: G = 8192 ladders per
+GPU, each the paper's alpha = 1..4 ladder at a seeded base eps
+(log-uniform in [5e-4, 5e-3], around the paper's 2e-3), K = 8G = 65536
+signed lanes, R = 1, one recovered solution per ladder.  Weak scaling: every rank
+owns its own 8192 ladders (no data-path collective: ladders are whole per rank).
+The 2.9 GB factor written every step is > 126 MB L2, so no explicit L2 flush.
+
+Contract: see the task's bench.py spec; prints ONE JSON line on rank 0.
+`--impl reference` times the CPU oracle (the baseline arm of this tier).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+from psp_inputs import Workload, integer_ladder  # noqa: E402
+
+G_PER_GPU = 8192
+M_LADDER = 4
+
+
+def bench_workload(rank: int = 0, G: int = G_PER_GPU) -> Workload:
+    rng = np.random.default_rng([0, 7, rank])
+    base = 10.0 ** rng.uniform(np.log10(5e-4), np.log10(5e-3), G)
+    return Workload("cfg1-300bus-batchK", 300, 411, 69, 1,
+                    [integer_ladder(e, M_LADDER) for e in base])
+
+
+def _json_print(d):
+    print(json.dumps(d), flush=True)
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as fh:
+            for line in fh:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 7:
+                    rows.append(parts)
+        os.unlink(self.f.name)
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+def oracle_lanes(s, perm, eps, tol, threads=None):
+    import oracle
+    if threads:
+        oracle.set_num_threads(threads)
+    t0 = time.perf_counter()
+    X, st = oracle.dense_batch(s, perm, eps, tol)
+    return X, st, time.perf_counter() - t0, oracle.num_threads()
+
+
+def cpu_baseline(s, w, n_lanes):
+    """The oracle as it stands (dense OR1 + combination), on a bounded sample."""
+    import oracle
+    from oracle import ordering
+    perm = ordering.min_degree_order(s.n, s.row_ptr, s.col_idx)
+    tol = oracle.default_tol(s.n, s.row_ptr, s.col_idx, s.vals)
+    eps = w.eps()[:n_lanes]
+    X, st, dt, cores = oracle_lanes(s, perm, eps, tol)
+    t0 = time.perf_counter()
+    ladders = w.ladders[:n_lanes // (2 * M_LADDER)]
+    xo = oracle.combine(oracle.ladder_weight_matrix(ladders), X)
+    dt += time.perf_counter() - t0
+    return {"value": n_lanes / dt, "unit": "perturbed solves/s", "cores": cores, "kind": "oracle",
+            "sample": f"first {n_lanes} lanes ({len(ladders)} ladders) of the workload, dense OR1 "
+                      f"pivot-free GE + forward/back + combination, {dt:.2f} s"}, X, st, perm
+
+
+def run_reference(args):
+    """--impl reference: the oracle timed on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    w = bench_workload(0)
+    s = w.system()
+    import oracle
+    from oracle import ordering
+    perm = ordering.min_degree_order(s.n, s.row_ptr, s.col_idx)
+    tol = oracle.default_tol(s.n, s.row_ptr, s.col_idx, s.vals)
+    lanes = args.ref_lanes
+    eps_all = w.eps()
+    times = []
+    cores = oracle.num_threads()
+    for it in range(args.warmup + args.steps):
+        lo = (it * lanes) % len(eps_all)
+        eps = eps_all[lo:lo + lanes]
+        t0 = time.perf_counter()
+        X, st = oracle.dense_batch(s, perm, eps, tol)
+        lad = w.ladders[lo // (2 * M_LADDER): (lo + lanes) // (2 * M_LADDER)]
+        oracle.combine(oracle.ladder_weight_matrix(lad), X)
+        if it >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    t = sum(times)
+    value = lanes * args.steps / t
+    _json_print({
+        "impl": "reference", "metric": "perturbed solves/s", "value": value,
+        "unit": "perturbed solves/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w.name, "n": s.n, "nnz_A": s.nnz, "K_per_step": lanes, "R": 1,
+                   "ladder": f"alpha=1..{M_LADDER}", "parallelism": "cpu threads"},
+        "cpu_baseline": {"value": value, "unit": "perturbed solves/s", "cores": cores,
+                         "kind": "oracle",
+                         "sample": f"{lanes} lanes per step (bounded sample of the K=65536 batch)"},
+        "e2e": {"value": value, "unit": "perturbed solves/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    })
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="psp", choices=["psp", "reference"])
+    ap.add_argument("--ladders", type=int, default=G_PER_GPU, help="ladders per GPU")
+    ap.add_argument("--cpu-lanes", type=int, default=512, help="oracle sample for cpu_baseline")
+    ap.add_argument("--ref-lanes", type=int, default=256, help="oracle lanes per reference step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    from paper_2311_11833_b200 import psp
+
+    w = bench_workload(rank, args.ladders)
+    s = w.system()
+    eps = w.eps()
+    K = len(eps)
+    stream = torch.cuda.current_stream()
+    solver = psp.Solver(local_rank, stream)
+    t0 = time.perf_counter()
+    solver.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering="mindeg")
+    t_sym = time.perf_counter() - t0
+    info, perm = solver.psp_get_symbolic_info()
+    solver.psp_set_perturbations(eps, s.d)
+    wp, wl, wv = psp.ladder_weights_csr(w.ladders)
+    solver.psp_set_weights(wp, wl, wv)
+    W = len(w.ladders)
+    A = torch.tensor(s.vals, dtype=torch.float64, device="cuda")
+    B = torch.tensor(s.b.T.copy(), dtype=torch.float64, device="cuda")
+    xh = torch.empty((W, 1, s.n), dtype=torch.float64, device="cuda")
+
+    def step(ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        solver.psp_factor_batch(A, 0.0)
+        if ev is not None:
+            ev[1].record(stream)
+        solver.psp_solve_batch(B)
+        if ev is not None:
+            ev[2].record(stream)
+        solver.psp_recover(xh)
+        if ev is not None:
+            ev[3].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    rc, st = solver.psp_get_lane_status()
+    n_failed = int((st != 0).sum())
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    clk = ClockSampler(local_rank) if rank == 0 else None
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for i in range(args.steps):
+        step(evs[i])
+    end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop() if clk else None
+    ms_total = start.elapsed_time(end)
+    t_factor = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
+    t_solve = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
+    t_recover = sum(e[2].elapsed_time(e[3]) for e in evs) / args.steps
+    if world > 1:
+        tt = torch.tensor([ms_total], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_total = float(tt.item())
+
+    # ---- e2e through the host-buffer C-ABI call -------------------------------
+    A_h = torch.tensor(s.vals, dtype=torch.float64).pin_memory()
+    B_h = torch.tensor(s.b.T.copy(), dtype=torch.float64).pin_memory()
+    x_h = torch.empty((W, 1, s.n), dtype=torch.float64).pin_memory()
+    for _ in range(2):
+        solver.psp_solve_host(A_h, B_h, x_h)
+    e2e_steps = max(3, min(args.steps, 10))
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        solver.psp_solve_host(A_h, B_h, x_h)
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        tt = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    e2e_ok = bool(np.array_equal(x_h.numpy(), xh.cpu().numpy()))
+
+    if rank == 0:
+        nnzLU, n, R = info["nnz_LU"], s.n, 1
+        # algorithmic bytes per launch: the factor kernel's output is the
+        # 8*nnz_LU values of every lane (A and eps/d reads are shared and negligible)
+        bytes_factor = 8.0 * nnzLU * K + 8.0 * s.nnz + 16.0 * K
+        bytes_solve = 8.0 * nnzLU * K + 8.0 * n * R * K + 8.0 * n * R
+        bytes_recover = 8.0 * n * R * K + 8.0 * W * R * n
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
+            if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+        peak = peaks.get("hbm_gbs", 6650.0)
+        peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+        kern = {"factor": (t_factor, bytes_factor), "solve": (t_solve, bytes_solve),
+                "recover": (t_recover, bytes_recover)}
+        dom = max(kern, key=lambda k: kern[k][0])
+        tdom, bdom = kern[dom]
+        achieved = bdom / (tdom * 1e-3) / 1e9
+        ms_step = ms_total / args.steps
+        total_lanes = K * world * args.steps
+        value = total_lanes / (ms_total * 1e-3)
+        rec_value = W * R * world * args.steps / (ms_total * 1e-3)
+        out = {
+            "metric": "perturbed solves/s", "value": value, "unit": "perturbed solves/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": w.name, "n": n, "nnz_A": s.nnz, "nnz_LU": nnzLU,
+                       "K_per_gpu": K, "R": R, "W_per_gpu": W,
+                       "ladder": f"alpha=1..{M_LADDER}, base eps log-uniform [5e-4,5e-3]",
+                       "ordering": "mindeg", "parallelism": f"perturbation-batch dp{world}",
+                       "l2": "no flush: 2.9 GB factor written per step > 126 MB L2"},
+            "recovered_solves_per_s": rec_value,
+            "phases_ms": {"factor": t_factor, "solve": t_solve, "recover": t_recover,
+                          "symbolic_once": 1e3 * t_sym},
+            "hbm_gbs_algorithmic": (bytes_factor + bytes_solve + bytes_recover) / (ms_step * 1e-3) / 1e9,
+            "roofline": {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                         "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": bdom, "launch_ms": tdom},
+            "gpu_launches": 4 * args.steps,
+            "clocks": clocks,
+            "lane_failures": n_failed,
+            "symbolic": info,
+        }
+        h2d = 8 * s.nnz + 8 * n * R
+        d2h = 8 * W * R * n
+        out["e2e"] = {"value": K * world * e2e_steps / e2e_s, "unit": "perturbed solves/s",
+                      "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                      "ms_per_step": 1e3 * e2e_s / e2e_steps, "matches_device_result": e2e_ok}
+        if not args.no_cpu_baseline:
+            cb, Xo, sto, operm = cpu_baseline(s, w, args.cpu_lanes)
+            out["cpu_baseline"] = cb
+            Xg = solver.psp_get_solutions()[: args.cpu_lanes].cpu().numpy()
+            ok = sto == 0
+            same_perm = bool(np.array_equal(operm, perm))
+            err = float(np.max(np.abs(Xg[ok] - Xo[ok]) / np.maximum(np.abs(Xo[ok]), 1e-300))) \
+                if ok.any() else None
+            out["rel_err_vs_oracle"] = {"max_rel_lane": err, "lanes_checked": int(ok.sum()),
+                                        "bitwise": bool(np.array_equal(Xg[ok], Xo[ok])),
+                                        "same_order": same_perm}
+        _json_print(out)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    solver.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,199 @@
+/*
+ * psp.h — C ABI of the B200-native batched perturbation-induced static-pivoting
+ * solver (arXiv 2311.11833, "Towards Perturbation-Induced Static Pivoting on
+ * GPU-Based Linear Solvers"; PAPER.md = /root/reference/PAPER.md, line refs P:Lnnn).
+ *
+ * The library solves one sparse system A x = b by solving K diagonally perturbed
+ * copies  A_k = A + eps_k * D  (D = diag(d)) WITHOUT pivoting — all copies share
+ * one symbolic pattern and one static elimination order — and recombining the K
+ * solutions with the paper's weights (Alg. 1):
+ *
+ *   psp_symbolic_analyse   once per sparsity pattern (host; ordering, fill, plans)
+ *   psp_set_perturbations  signed eps_k per lane and d          (Alg. 1 step 1)
+ *   psp_factor_batch       batched pivot-free numeric LU         (Alg. 1 step 2)
+ *   psp_solve_batch        batched forward/back substitution     (Alg. 1 step 2)
+ *   psp_set_weights +
+ *   psp_recover            x_hat[w] = sum_k w[w][k] x_k          (Alg. 1 steps 3-4,
+ *                                                                 Eq. (13)/(14))
+ *
+ * Conventions (all functions):
+ *  - Every function returns psp_status (PSP_OK == 0).  Arguments are validated
+ *    before any device work; on error nothing is launched and the handle state
+ *    is unchanged (except psp_destroy).  psp_last_error_detail() gives a message.
+ *  - Pointers suffixed _h are HOST memory.  Every other pointer is DEVICE memory
+ *    of the handle's device.  Calls are stream-ordered on the handle's stream
+ *    (like cuBLAS): device inputs must stay valid until the stream reaches the
+ *    operation; the library never retains a caller pointer past the call (it
+ *    copies patterns, eps, d and weights into its own memory).
+ *  - Floating point is IEEE binary64.  Each lane's arithmetic is performed in the
+ *    canonical order of DESIGN.md R11/R12 (one fma per "a - l*u" update, updates
+ *    to each entry in ascending pivot order, forward substitution ascending,
+ *    backward descending, true division), so per-lane results are bitwise
+ *    reproducible and independent of K, the lane's position and the GPU count.
+ *  - Handles are not thread-safe; distinct handles are independent.
+ */
+#ifndef PSP_H_
+#define PSP_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct psp_ctx* psp_handle;
+typedef int32_t psp_status;
+
+enum {
+  PSP_OK = 0,
+  PSP_ERR_ARG = 1,               /* NULL / out-of-range argument, malformed pattern */
+  PSP_ERR_DIM = 2,               /* sizes inconsistent with the analysed pattern    */
+  PSP_ERR_STATE = 3,             /* call order violated (e.g. factor before set_perturbations) */
+  PSP_ERR_ZERO_PIVOT = 4,        /* >= 1 lane hit |u_pp| <= tol or a non-finite pivot
+                                    (SPEC S:L46 ZeroPivot; P:L304 failure mode).  The
+                                    batch is still complete; see per-lane status.     */
+  PSP_ERR_BATCH_INFEASIBLE = 5,  /* a non-zero weight touches a failed lane */
+  PSP_ERR_CUDA = 6,              /* CUDA runtime error; detail string has the code   */
+  PSP_ERR_ALLOC = 7,             /* device or host allocation failed                 */
+  PSP_ERR_UNSUPPORTED = 8        /* feature not available in this build              */
+};
+
+/* Elimination orders for psp_symbolic_analyse (R13). */
+enum {
+  PSP_ORDER_NATURAL = 0,         /* the given order                                  */
+  PSP_ORDER_MINDEG = 1,          /* exact minimum degree on pattern(A+A^T), ties to
+                                    the lowest original index                        */
+  PSP_ORDER_USER = 2,            /* user_perm_h[new] = old                          */
+  PSP_ORDER_MINDEG_FIRST = 3     /* eliminate `first_node` first, then MINDEG: the
+                                    'leading-zero' regime of P:L304                  */
+};
+
+typedef struct {
+  int32_t n;                     /* matrix dimension                                 */
+  int32_t nnz_A;                 /* stored entries of A                              */
+  int32_t nnz_LU;                /* slots of the filled L+U pattern (incl. diagonal) */
+  int32_t nnz_L;                 /* strictly-lower slots                             */
+  int32_t n_struct_zero_diag;    /* diagonal positions absent from A's pattern       */
+  int32_t n_levels;              /* elimination-tree height (levels of the schedule) */
+  int64_t factor_fma;            /* fused multiply-adds per lane in the factorisation */
+  int64_t factor_div;            /* divisions per lane (strictly-lower slots)        */
+  int64_t solve_fma;             /* fmas per lane per right-hand side (fwd + bwd)    */
+  int32_t max_live;              /* max simultaneously-live L values per lane (plan) */
+  int32_t kernel_variant;        /* factor kernel chosen by the plan  */
+} psp_symbolic_info;
+
+/* ---- lifetime ---------------------------------------------------------------- */
+
+/* Create a handle bound to CUDA device `device` and stream `cuda_stream`
+ * (a cudaStream_t; NULL = the legacy default stream).  *out receives the handle.
+ * device < 0 creates a HOST-ONLY handle: psp_symbolic_analyse and
+ * psp_get_symbolic_info work (no device plans are uploaded); every numeric call
+ * returns PSP_ERR_UNSUPPORTED or PSP_ERR_STATE.  Errors: ARG, CUDA (bad device). */
+psp_status psp_create(psp_handle* out, int32_t device, void* cuda_stream);
+
+/* Release all device and host memory of the handle (synchronises its stream). */
+psp_status psp_destroy(psp_handle h);
+
+/* Rebind the handle to another stream of the same device. */
+psp_status psp_set_stream(psp_handle h, void* cuda_stream);
+
+const char* psp_status_string(psp_status s);
+const char* psp_last_error_detail(psp_handle h);
+
+/* ---- symbolic analysis (a static pivot sequence "computed once, and
+ *      perpetually reused"; host-side, once per pattern) ---------------------- */
+
+/* Analyse the pattern of the n x n CSR matrix A (row_ptr_h[n+1], col_idx_h[nnz];
+ * column indices strictly increasing within each row, no duplicates).  Computes
+ * the elimination order (`ordering`, see enum; user_perm_h[n] for USER, else may
+ * be NULL; first_node for MINDEG_FIRST, else ignored), the filled L+U pattern of
+ * pattern(A + A^T + I), the batch-major slot layout and the device plans.
+ * Discards any previous analysis, perturbations, weights and results.
+ * Errors: PSP_ERR_ARG (malformed pattern / permutation), PSP_ERR_ALLOC. */
+psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_h,
+                                const int32_t* col_idx_h, int32_t ordering,
+                                const int32_t* user_perm_h, int32_t first_node);
+
+/* Statistics of the analysis; perm_h (may be NULL) receives perm[new] = old. */
+psp_status psp_get_symbolic_info(psp_handle h, psp_symbolic_info* info_h, int32_t* perm_h);
+
+/* ---- perturbations (Alg. 1 step 1; Eqs. (5)-(6)) ---------- */
+
+/* Set the K lanes this handle owns: lane k solves (A + eps_h[k] * diag(d_h)) x = b.
+ * eps_h[K] are the signed perturbations (e.g. the ladder [+s1,-s1,+s2,-s2,...]
+ * with s_j = alpha_j * eps); d_h[n] is D's diagonal in the ORIGINAL
+ * ordering (the paper scales ||D||_1 = max|d_i| = 1; the library does not
+ * rescale).  The perturbed diagonal entry is a_ii + (eps_k * d_i) (two roundings).
+ * Allocates the batch-major factor storage (8 * nnz_LU * K bytes).  A multi-GPU
+ * caller passes only its shard of eps.  Errors: ARG, STATE, ALLOC. */
+psp_status psp_set_perturbations(psp_handle h, int32_t K, const double* eps_h, const double* d_h);
+
+/* ---- numeric phase ------------------------------------------------------------ */
+
+/* Batched pivot-free LU (Alg. 1 step 2; the getrf_batched of P:L310 made
+ * sparse).  A_vals[nnz_A] (device) are A's values in the CSR order given to
+ * psp_symbolic_analyse.  pivot_tol > 0: a pivot with |u_pp| <= pivot_tol or a
+ * non-finite pivot fails the lane; pivot_tol <= 0 selects n * 2^-52 * ||A||_1
+ * (SPEC S:L95), computed on the device from A_vals.  Per-lane status (0 ok, else
+ * 1 + first failing permuted pivot position) is kept on the device; if
+ * lane_status is non-NULL (device int32[K]) it is also written there.  Failed
+ * lanes do not stop the batch.  Asynchronous: returns PSP_OK without checking
+ * statuses (use psp_get_lane_status).  Errors: ARG, STATE, CUDA. */
+psp_status psp_factor_batch(psp_handle h, const double* A_vals, double pivot_tol,
+                            int32_t* lane_status);
+
+/* Batched forward (unit L, ascending) and backward (U, descending) substitution
+ * for R right-hand sides shared by all lanes (Alg. 1 step 2; the trsm pair of
+ * P:L310).  B (device) is n x R column-major with leading dimension ldb >= n, in
+ * the ORIGINAL ordering.  Solutions stay in library memory (see psp_get_solutions).
+ * Errors: ARG, STATE, ALLOC, CUDA. */
+psp_status psp_solve_batch(psp_handle h, int32_t R, const double* B, int64_t ldb);
+
+/* Copy the per-lane solutions to X (device, K x R x n, lane-major, ORIGINAL
+ * ordering): X[(k*R + r)*n + i] = x_k,r[i].  Errors: ARG, STATE. */
+psp_status psp_get_solutions(psp_handle h, double* X);
+
+/* Recombination weights (Remark 2 / Eq. (13), with the pair average of
+ * Eq. (avg_hats), folded in: weight beta_j / 2 on each sign).  CSR over
+ * W recovered solutions: entries w_ptr_h[w]..w_ptr_h[w+1]-1 list local lanes
+ * w_lane_h[] (strictly ascending within a row, 0 <= lane < K) and weights w_val_h[].
+ * Exact-zero weights are dropped.  Copied to the device.  Errors: ARG, STATE. */
+psp_status psp_set_weights(psp_handle h, int32_t W, const int32_t* w_ptr_h,
+                           const int32_t* w_lane_h, const double* w_val_h);
+
+/* x[(w*R + r)*n + i] = sum over the row's lanes k (ascending) of w * x_k,r[i]
+ * (ORIGINAL ordering; one fma per term, Alg. 1 steps 3-4).  x is device memory
+ * W x R x n.  With lanes sharded across GPUs this is the rank-local partial sum;
+ * the caller reduces it (sum) across ranks.  A non-zero weight on a failed lane
+ * yields NaN for that solution and raises the batch-infeasible flag
+ * (psp_get_lane_status).  Errors: ARG, STATE, CUDA. */
+psp_status psp_recover(psp_handle h, double* x);
+
+/* Synchronise the stream and copy per-lane status to status_h[K] (may be NULL).
+ * Returns PSP_ERR_BATCH_INFEASIBLE if the last psp_recover raised its flag, else
+ * PSP_ERR_ZERO_PIVOT if any lane failed, else PSP_OK. */
+psp_status psp_get_lane_status(psp_handle h, int32_t* status_h);
+
+/* End-to-end call with HOST buffers (the e2e path): copies A_vals_h[nnz_A] and
+ * B_h (n x R col-major) to the device, runs factor (pivot_tol as above), solve and
+ * recover, copies x_h[W x R x n] back and synchronises.  Pinned host memory gives
+ * asynchronous copies; pageable works.  Returns like psp_get_lane_status. */
+psp_status psp_solve_host(psp_handle h, const double* A_vals_h, int32_t R, const double* B_h,
+                          double pivot_tol, double* x_h);
+
+/* Synchronise the handle's stream. */
+psp_status psp_synchronize(psp_handle h);
+
+/* ---- host helper (pure) --------------------------------------------------------- */
+
+/* Paper ladder (Remark 2): for m magnitudes s_h[j] (distinct, non-zero),
+ * eps_out_h[2m] = [+s_1, -s_1, ..., +s_m, -s_m] and w_out_h[2m] = beta_j / 2 on both
+ * signs, beta_j = prod_{l != j} s_l^2 / (s_l^2 - s_j^2) (the solution of
+ * Gamma_m^T beta = e_1, computed in long double without forming Gamma).
+ * Errors: ARG (m < 1, m > 64, repeated or zero magnitude). */
+psp_status psp_ladder_weights(int32_t m, const double* s_h, double* eps_out_h, double* w_out_h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PSP_H_ */

@@ -1,0 +1,268 @@
+"""Thin ctypes binding of libpsp.so (include/psp.h).  Argument marshalling only:
+every numeric step runs in the library's CUDA kernels; there is no CPU fallback.
+Functions keep the C names; `Solver` is a convenience wrapper over them that takes
+torch tensors for device buffers (torch supplies memory and streams only)."""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpsp.so")
+
+PSP_OK = 0
+STATUS = {0: "PSP_OK", 1: "PSP_ERR_ARG", 2: "PSP_ERR_DIM", 3: "PSP_ERR_STATE",
+          4: "PSP_ERR_ZERO_PIVOT", 5: "PSP_ERR_BATCH_INFEASIBLE", 6: "PSP_ERR_CUDA",
+          7: "PSP_ERR_ALLOC", 8: "PSP_ERR_UNSUPPORTED"}
+PSP_ERR_ZERO_PIVOT = 4
+PSP_ERR_BATCH_INFEASIBLE = 5
+ORDER = {"natural": 0, "mindeg": 1, "user": 2, "mindeg_first": 3}
+
+EXPORTS = ["psp_create", "psp_destroy", "psp_set_stream", "psp_status_string",
+           "psp_last_error_detail", "psp_symbolic_analyse", "psp_get_symbolic_info",
+           "psp_set_perturbations", "psp_factor_batch", "psp_solve_batch", "psp_get_solutions",
+           "psp_set_weights", "psp_recover", "psp_get_lane_status", "psp_solve_host",
+           "psp_synchronize", "psp_ladder_weights"]
+
+
+class SymbolicInfo(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("nnz_A", ctypes.c_int32), ("nnz_LU", ctypes.c_int32),
+                ("nnz_L", ctypes.c_int32), ("n_struct_zero_diag", ctypes.c_int32),
+                ("n_levels", ctypes.c_int32), ("factor_fma", ctypes.c_int64),
+                ("factor_div", ctypes.c_int64), ("solve_fma", ctypes.c_int64),
+                ("max_live", ctypes.c_int32), ("kernel_variant", ctypes.c_int32)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class PSPError(RuntimeError):
+    def __init__(self, status, detail=""):
+        super().__init__(f"{STATUS.get(status, status)}: {detail}")
+        self.status = status
+
+
+_lib = None
+
+
+def lib():
+    """Load libpsp.so; fails loudly when the CUDA library is missing (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(LIB_PATH)
+        P, I32, I64, D = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+        sig = {
+            "psp_create": [ctypes.POINTER(P), I32, P],
+            "psp_destroy": [P],
+            "psp_set_stream": [P, P],
+            "psp_synchronize": [P],
+            "psp_symbolic_analyse": [P, I32, P, P, I32, P, I32],
+            "psp_get_symbolic_info": [P, ctypes.POINTER(SymbolicInfo), P],
+            "psp_set_perturbations": [P, I32, P, P],
+            "psp_factor_batch": [P, P, D, P],
+            "psp_solve_batch": [P, I32, P, I64],
+            "psp_get_solutions": [P, P],
+            "psp_set_weights": [P, I32, P, P, P],
+            "psp_recover": [P, P],
+            "psp_get_lane_status": [P, P],
+            "psp_solve_host": [P, P, I32, P, D, P],
+            "psp_ladder_weights": [I32, P, P, P],
+        }
+        for name, args in sig.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = I32
+        L.psp_status_string.argtypes = [I32]
+        L.psp_status_string.restype = ctypes.c_char_p
+        L.psp_last_error_detail.argtypes = [P]
+        L.psp_last_error_detail.restype = ctypes.c_char_p
+        _lib = L
+    return _lib
+
+
+def _np_ptr(a):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _t_ptr(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def psp_ladder_weights(magnitudes):
+    """C helper: (eps[2m], w[2m]) for one ladder (Remark 2, beta/2 per sign)."""
+    s = np.ascontiguousarray(magnitudes, dtype=np.float64)
+    m = len(s)
+    eps = np.empty(2 * m)
+    w = np.empty(2 * m)
+    st = lib().psp_ladder_weights(m, _np_ptr(s), _np_ptr(eps), _np_ptr(w))
+    if st:
+        raise PSPError(st, "psp_ladder_weights")
+    return eps, w
+
+
+class Solver:
+    """Owns one psp_handle on `device` / `stream` (a torch.cuda.Stream or None)."""
+
+    def __init__(self, device=0, stream=None):
+        import torch
+        self.torch = torch
+        self.device = device
+        self.stream = stream if stream is not None else torch.cuda.current_stream(device)
+        h = ctypes.c_void_p()
+        self._check(lib().psp_create(ctypes.byref(h), device, ctypes.c_void_p(self.stream.cuda_stream)))
+        self.h = h
+        self.n = self.K = self.W = 0
+
+    def _check(self, st):
+        if st != PSP_OK:
+            det = ""
+            if getattr(self, "h", None) is not None and self.h:
+                det = lib().psp_last_error_detail(self.h).decode()
+            raise PSPError(st, det)
+        return st
+
+    def close(self):
+        if getattr(self, "h", None) is not None and self.h:
+            lib().psp_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    # --- C-ABI wrappers ------------------------------------------------------
+    def psp_symbolic_analyse(self, n, row_ptr, col_idx, ordering="mindeg", user_perm=None, first_node=-1):
+        rp = np.ascontiguousarray(row_ptr, dtype=np.int32)
+        ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+        up = None if user_perm is None else np.ascontiguousarray(user_perm, dtype=np.int32)
+        self._check(lib().psp_symbolic_analyse(self.h, int(n), _np_ptr(rp), _np_ptr(ci), ORDER[ordering],
+                                               None if up is None else _np_ptr(up), int(first_node)))
+        self.n = int(n)
+        self.nnz_A = int(rp[-1])
+
+    def psp_get_symbolic_info(self):
+        info = SymbolicInfo()
+        perm = np.empty(self.n, dtype=np.int32)
+        self._check(lib().psp_get_symbolic_info(self.h, ctypes.byref(info), _np_ptr(perm)))
+        return info.as_dict(), perm
+
+    def psp_set_perturbations(self, eps, d):
+        e = np.ascontiguousarray(eps, dtype=np.float64)
+        dd = np.ascontiguousarray(d, dtype=np.float64)
+        if dd.shape != (self.n,):
+            raise ValueError("d must have n entries")
+        self._check(lib().psp_set_perturbations(self.h, len(e), _np_ptr(e), _np_ptr(dd)))
+        self.K = len(e)
+
+    def psp_factor_batch(self, A_vals, pivot_tol=0.0, lane_status=None):
+        self._check_dev(A_vals, self.torch.float64, (self.nnz_A,))
+        ls = None
+        if lane_status is not None:
+            self._check_dev(lane_status, self.torch.int32, (self.K,))
+            ls = _t_ptr(lane_status)
+        self._check(lib().psp_factor_batch(self.h, _t_ptr(A_vals), float(pivot_tol), ls))
+
+    def psp_solve_batch(self, B):
+        """B: device float64 [R, n] (row r = RHS r; equals n x R column-major)."""
+        self._check_dev(B, self.torch.float64, None)
+        R, n = B.shape
+        assert n == self.n and B.is_contiguous()
+        self._check(lib().psp_solve_batch(self.h, R, _t_ptr(B), n))
+        self.R = R
+
+    def psp_get_solutions(self, out=None):
+        out = out if out is not None else self.torch.empty((self.K, self.R, self.n), dtype=self.torch.float64,
+                                                           device=f"cuda:{self.device}")
+        self._check(lib().psp_get_solutions(self.h, _t_ptr(out)))
+        return out
+
+    def psp_set_weights(self, w_ptr, w_lane, w_val):
+        p = np.ascontiguousarray(w_ptr, dtype=np.int32)
+        la = np.ascontiguousarray(w_lane, dtype=np.int32)
+        v = np.ascontiguousarray(w_val, dtype=np.float64)
+        self._check(lib().psp_set_weights(self.h, len(p) - 1, _np_ptr(p), _np_ptr(la), _np_ptr(v)))
+        self.W = len(p) - 1
+
+    def psp_recover(self, out=None):
+        out = out if out is not None else self.torch.empty((self.W, self.R, self.n), dtype=self.torch.float64,
+                                                           device=f"cuda:{self.device}")
+        self._check(lib().psp_recover(self.h, _t_ptr(out)))
+        return out
+
+    def psp_get_lane_status(self):
+        st = np.empty(self.K, dtype=np.int32)
+        rc = lib().psp_get_lane_status(self.h, _np_ptr(st))
+        if rc not in (PSP_OK, PSP_ERR_ZERO_PIVOT, PSP_ERR_BATCH_INFEASIBLE):
+            self._check(rc)
+        return rc, st
+
+    def psp_solve_host(self, A_vals_h, B_h, x_h, pivot_tol=0.0):
+        """Host-buffer end-to-end call (torch CPU tensors, ideally pinned)."""
+        R = B_h.shape[0]
+        rc = lib().psp_solve_host(self.h, _t_ptr(A_vals_h), R, _t_ptr(B_h), float(pivot_tol), _t_ptr(x_h))
+        if rc not in (PSP_OK, PSP_ERR_ZERO_PIVOT, PSP_ERR_BATCH_INFEASIBLE):
+            self._check(rc)
+        self.R = R
+        return rc
+
+    def psp_synchronize(self):
+        self._check(lib().psp_synchronize(self.h))
+
+    def _check_dev(self, t, dtype, shape):
+        if not t.is_cuda or t.dtype != dtype or not t.is_contiguous():
+            raise ValueError(f"expected a contiguous CUDA {dtype} tensor")
+        if shape is not None and tuple(t.shape) != shape:
+            raise ValueError(f"expected shape {shape}, got {tuple(t.shape)}")
+
+
+def ladder_weights_csr(ladders, lane_offset=0, k_begin=0, k_end=None):
+    """Weights CSR for ladders laid out consecutively in lane order (one recovered
+    solution per ladder).  Only lanes in [k_begin, k_end) are kept, renumbered to
+    local lanes (multi-GPU sharding: each rank recovers its own partial sums)."""
+    ptr, lane, val = [0], [], []
+    k = lane_offset
+    for mags in ladders:
+        _, w = psp_ladder_weights(mags)
+        for j, c in enumerate(w):
+            kk = k + j
+            if k_end is None or (k_begin <= kk < k_end):
+                lane.append(kk - k_begin)
+                val.append(c)
+        k += len(w)
+        ptr.append(len(lane))
+    return np.array(ptr, np.int32), np.array(lane, np.int32), np.array(val, np.float64)
+
+
+class HostSymbolic:
+    """Host-only handle (psp_create with device = -1): symbolic analysis only."""
+
+    def __init__(self):
+        h = ctypes.c_void_p()
+        st = lib().psp_create(ctypes.byref(h), -1, None)
+        if st:
+            raise PSPError(st, "psp_create(host-only)")
+        self.h = h
+
+    def analyse(self, n, row_ptr, col_idx, ordering="mindeg", user_perm=None, first_node=-1):
+        rp = np.ascontiguousarray(row_ptr, dtype=np.int32)
+        ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+        up = None if user_perm is None else np.ascontiguousarray(user_perm, dtype=np.int32)
+        st = lib().psp_symbolic_analyse(self.h, int(n), _np_ptr(rp), _np_ptr(ci), ORDER[ordering],
+                                        None if up is None else _np_ptr(up), int(first_node))
+        if st:
+            raise PSPError(st, lib().psp_last_error_detail(self.h).decode())
+        info = SymbolicInfo()
+        perm = np.empty(int(n), dtype=np.int32)
+        st = lib().psp_get_symbolic_info(self.h, ctypes.byref(info), _np_ptr(perm))
+        if st:
+            raise PSPError(st, "psp_get_symbolic_info")
+        return info.as_dict(), perm
+
+    def close(self):
+        if self.h:
+            lib().psp_destroy(self.h)
+            self.h = None
+
+    __del__ = close

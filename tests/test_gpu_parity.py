@@ -1,0 +1,249 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by
+element on the same seeded inputs.
+
+Bar (BASELINE north_star): per-lane solutions within 1e-11 relative
+— the kernels keep the canonical operation order, so they are asserted BITWISE
+equal; recovered x within 1e-10 relative of the oracle's recovered x; statuses
+(integers) bit-exact.  Sizes: the oracle runs every lane where it finishes in
+seconds (configs 0-1, ragged K), sampled lanes at the full BASELINE sizes."""
+import numpy as np
+import pytest
+
+import oracle
+from oracle import ordering
+from psp_inputs import config, ladder_eps
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2311_11833_b200 import psp  # noqa: E402
+
+
+def gpu_run(s, eps, ordering_kind="mindeg", first=-1, tol=0.0, B=None, ladders=None,
+            w_csr=None, lanes_out=True):
+    solver = psp.Solver(0)
+    solver.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering=ordering_kind, first_node=first)
+    info, perm = solver.psp_get_symbolic_info()
+    # the oracle's own elimination order (never the product's): integer parity
+    if ordering_kind == "natural":
+        operm = np.arange(s.n, dtype=np.int32)
+    else:
+        operm = ordering.min_degree_order(s.n, s.row_ptr, s.col_idx, first=None if first < 0 else first)
+    assert np.array_equal(perm, operm)
+    solver.psp_set_perturbations(eps, s.d)
+    A = torch.tensor(s.vals, dtype=torch.float64, device="cuda")
+    st = torch.empty(len(eps), dtype=torch.int32, device="cuda")
+    solver.psp_factor_batch(A, tol, st)
+    Bt = torch.tensor((s.b if B is None else B).T.copy(), dtype=torch.float64, device="cuda")
+    solver.psp_solve_batch(Bt)
+    X = solver.psp_get_solutions() if lanes_out else None
+    xh = None
+    if ladders is not None or w_csr is not None:
+        wp, wl, wv = w_csr if w_csr is not None else psp.ladder_weights_csr(ladders)
+        solver.psp_set_weights(wp, wl, wv)
+        xh = solver.psp_recover()
+    torch.cuda.synchronize()
+    rc, st_h = solver.psp_get_lane_status()
+    out = dict(perm=perm, operm=operm, info=info, status=st.cpu().numpy(), status_h=st_h, rc=rc,
+               X=None if X is None else X.cpu().numpy(),
+               xhat=None if xh is None else xh.cpu().numpy(), solver=solver)
+    return out
+
+
+def oracle_perm(s, first):
+    return ordering.min_degree_order(s.n, s.row_ptr, s.col_idx, first=None if first < 0 else first)
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+@pytest.mark.parametrize("ci", [0, 1])
+@pytest.mark.parametrize("leading_zero", [False, True])
+def test_full_parity_small_configs(ci, leading_zero):
+    w = config(ci)
+    s = w.system()
+    first = s.slot_p if leading_zero else -1
+    tol = oracle.default_tol(s.n, s.row_ptr, s.col_idx, s.vals)
+    eps = w.eps()
+    g = gpu_run(s, eps, "mindeg_first" if leading_zero else "mindeg", first, tol, ladders=w.ladders)
+    perm = oracle_perm(s, first)
+    assert np.array_equal(g["perm"], perm)
+    Xo, sto = oracle.dense_batch(s, perm, eps, tol)
+    assert np.array_equal(g["status"], sto) and np.array_equal(g["status_h"], sto)
+    assert (sto == 0).all()
+    assert np.array_equal(g["X"], Xo)                                   # bitwise per lane
+    xo = oracle.combine(oracle.ladder_weight_matrix(w.ladders), Xo)
+    assert rel(g["xhat"], xo) <= 1e-10
+    xs, _ = oracle.reference_solve(s)
+    assert rel(g["xhat"][0, 0], xs[0]) <= 1e-9                        # truncation + rounding
+
+
+@pytest.mark.parametrize("K", [1, 5, 37, 64, 100])
+def test_ragged_batches(K):
+    s = config(1).system()
+    rng = np.random.default_rng(K)
+    eps = rng.choice([-1, 1], K) * 10.0 ** rng.uniform(-6, -1, K)
+    tol = 1e-14
+    g = gpu_run(s, eps, tol=tol)
+    Xo, sto = oracle.dense_batch(s, g["operm"], eps, tol) if K <= 40 else \
+        oracle.SparseOracle(s, g["operm"]).batch(eps, tol)
+    assert np.array_equal(g["status"], sto)
+    ok = sto == 0
+    assert np.array_equal(g["X"][ok], Xo[ok])
+
+
+def test_multi_rhs_and_leading_zero_extreme_eps():
+    from psp_inputs import build_system
+    s = build_system(300, 411, 69, seed=0, R=3)
+    eps = np.array([1e-2, -1e-2, 1e-4, -1e-4, 1e-6, -1e-6, 1e-8, -1e-8])
+    tol = 1e-300
+    g = gpu_run(s, eps, "mindeg_first", s.slot_p, tol)
+    Xo, sto = oracle.SparseOracle(s, g["operm"]).batch(eps, tol)
+    assert np.array_equal(g["status"], sto)
+    assert np.array_equal(g["X"], Xo)      # bitwise even where growth ~1/eps (DESIGN R11)
+
+
+def test_failure_modes():
+    w = config(1)
+    s = w.system()
+    tol = oracle.default_tol(s.n, s.row_ptr, s.col_idx, s.vals)
+    # unperturbed pivot-free solve hits a leading zero -> status 1 (step 0)
+    eps = np.r_[0.0, w.eps()]
+    g = gpu_run(s, eps, "mindeg_first", s.slot_p, 0.0, ladders=None)
+    assert g["status"][0] == 1 and (g["status"][1:] == 0).all()
+    assert g["rc"] == psp.PSP_ERR_ZERO_PIVOT
+    # a non-zero weight on the failed lane -> BATCH_INFEASIBLE and NaN
+    wp = np.array([0, 2, 4], np.int32)
+    wl = np.array([0, 1, 1, 2], np.int32)
+    wv = np.array([0.5, 0.5, 0.5, 0.5])
+    g = gpu_run(s, eps, "mindeg_first", s.slot_p, 0.0, w_csr=(wp, wl, wv))
+    assert g["rc"] == psp.PSP_ERR_BATCH_INFEASIBLE
+    assert np.isnan(g["xhat"][0]).all() and np.isfinite(g["xhat"][1]).all()
+    # literal variable order (negative control): statuses equal the oracle's
+    sl = w.system(convention="listed")
+    eps2 = np.array([0.0, 2e-3, -2e-3])
+    g = gpu_run(sl, eps2, "natural", -1, tol)
+    _, sto = oracle.SparseOracle(sl, np.arange(sl.n, dtype=np.int32)).batch(eps2, tol)
+    assert np.array_equal(g["status"], sto) and g["status"][0] != 0
+
+
+def test_default_pivot_tol_and_lane_independence():
+    w = config(1)
+    s = w.system()
+    eps = w.eps()
+    g1 = gpu_run(s, eps)                       # pivot_tol <= 0: device-computed default
+    # the same lanes at other batch positions (another slab, another warp lane)
+    eps2 = np.r_[np.full(45, 3e-3), eps[::-1]]
+    g2 = gpu_run(s, eps2)
+    assert np.array_equal(g2["X"][45:][::-1], g1["X"])
+    assert (g1["status"] == 0).all()
+
+
+def test_host_api_e2e_matches_device_path():
+    w = config(1, n_ladders=4)
+    s = w.system()
+    eps = w.eps()
+    g = gpu_run(s, eps, ladders=w.ladders)
+    solver = g["solver"]
+    A_h = torch.tensor(s.vals, dtype=torch.float64).pin_memory()
+    B_h = torch.tensor(s.b.T.copy(), dtype=torch.float64).pin_memory()
+    x_h = torch.empty((len(w.ladders), 1, s.n), dtype=torch.float64).pin_memory()
+    rc = solver.psp_solve_host(A_h, B_h, x_h)
+    assert rc == 0
+    assert np.array_equal(x_h.numpy(), g["xhat"])
+
+
+@pytest.mark.parametrize("ci", [2])
+def test_cfg2_geometric_ladder_sampled(ci):
+    w = config(ci)
+    s = w.system()
+    eps = w.eps()
+    tol = oracle.default_tol(s.n, s.row_ptr, s.col_idx, s.vals)
+    g = gpu_run(s, eps, tol=tol, ladders=w.ladders)
+    assert (g["status"] == 0).all()
+    sample = np.array([0, 1, 2, 3, 127, 128, 254, 255])
+    Xo, sto = oracle.dense_batch(s, g["operm"], eps[sample], tol)
+    assert np.array_equal(g["X"][sample], Xo)
+    # recovered with all 128 pairs against the oracle's combination of the GPU-independent
+    # sparse oracle lanes (all 256 lanes via OR2, bitwise equal to OR1)
+    Xs, _ = oracle.SparseOracle(s, g["operm"]).batch(eps, tol)
+    xo = oracle.combine(oracle.ladder_weight_matrix(w.ladders), Xs)
+    assert rel(g["xhat"], xo) <= 1e-10
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("ci", [3, 4])
+def test_large_configs_sampled_lanes(ci):
+    w = config(ci)
+    s = w.system()
+    eps = w.eps()
+    tol = oracle.default_tol(s.n, s.row_ptr, s.col_idx, s.vals)
+    g = gpu_run(s, eps, tol=tol, ladders=w.ladders)
+    assert np.array_equal(g["perm"], oracle_perm(s, -1))
+    assert (g["status"] == 0).all()
+    K = len(eps)
+    sample = np.unique(np.r_[0, 1, 15, 16, K // 2, K // 2 + 1, K - 16, K - 1])
+    so = oracle.SparseOracle(s, g["operm"])
+    Xo, sto = so.batch(eps[sample], tol)
+    assert np.array_equal(g["X"][sample], Xo)
+    # recovered solution of the first and last ladder
+    for gi in [0, len(w.ladders) - 1]:
+        lo = 16 * gi
+        lanes = np.arange(lo, lo + 16)
+        Xl, _ = so.batch(eps[lanes], tol)
+        xo = oracle.combine(oracle.ladder_weight_matrix([w.ladders[gi]]), Xl)
+        assert rel(g["xhat"][gi], xo[0]) <= 1e-10
+
+
+def test_bench_size_sampled():
+    """The launch configuration bench.py times (300-bus, K = 65536, R = 1)."""
+    from bench import bench_workload
+    w = bench_workload()
+    s = w.system()
+    eps = w.eps()
+    g = gpu_run(s, eps, ladders=w.ladders, lanes_out=False)
+    assert (g["status"] == 0).all()
+    solver = g["solver"]
+    X = solver.psp_get_solutions()
+    K = len(eps)
+    sample = np.unique(np.r_[0, 1, 31, 32, 33, K // 3, K // 2, K - 33, K - 2, K - 1])
+    Xs = X[torch.tensor(sample, device="cuda")].cpu().numpy()
+    tol = oracle.default_tol(s.n, s.row_ptr, s.col_idx, s.vals)
+    Xo, sto = oracle.dense_batch(s, g["operm"], eps[sample], tol)
+    assert (sto == 0).all()
+    assert np.array_equal(Xs, Xo)
+    for gi in [0, len(w.ladders) // 2, len(w.ladders) - 1]:
+        lanes = np.arange(8 * gi, 8 * gi + 8)
+        Xl, _ = oracle.dense_batch(s, g["operm"], eps[lanes], tol)
+        xo = oracle.combine(oracle.ladder_weight_matrix([w.ladders[gi]]), Xl)
+        assert rel(g["xhat"][gi], xo[0]) <= 1e-10
+
+
+def test_diagonal_closed_form_at_full_size():
+    """n = 18000 diagonal A, D: recovered x against the componentwise closed form
+    (exact error identity, holds at any size)."""
+    from test_oracle_solve import _Tiny
+    n = 18000
+    rng = np.random.default_rng(21)
+    a = rng.uniform(1, 3, n) * rng.choice([-1, 1], n)
+    d = rng.normal(size=n)
+    d /= np.abs(d).max()
+    b = rng.normal(size=n)
+    sysm = _Tiny.__new__(_Tiny)
+    sysm.n = n
+    sysm.row_ptr = np.arange(n + 1, dtype=np.int32)
+    sysm.col_idx = np.arange(n, dtype=np.int32)
+    sysm.vals = a.copy()
+    sysm.d = d
+    sysm.b = b.reshape(n, 1)
+    m, e = 4, 2e-3
+    mags = [j * e for j in range(1, m + 1)]
+    g = gpu_run(sysm, ladder_eps(mags), "natural", ladders=[mags])
+    r = (d / a) ** 2
+    pred = np.ones(n) * (-1) ** m
+    for sm in mags:
+        pred *= sm * sm / (1 - sm * sm * r)
+    pred *= r ** m * (b / a)
+    err = (b / a) - g["xhat"][0, 0]
+    assert np.max(np.abs(err - pred)) <= 16 * np.finfo(float).eps * np.max(np.abs(b / a))
