@@ -104,7 +104,7 @@ def cpu_baseline(s, w, n_lanes):
     """The oracle as it stands (dense OR1 + combination), on a bounded sample."""
     import oracle
     from oracle import ordering
-    perm = ordering.min_degree_order(s.n, s.row_ptr, s.col_idx)
+    perm = ordering.elimination_order(s.n, s.row_ptr, s.col_idx)
     tol = oracle.default_tol(s.n, s.row_ptr, s.col_idx, s.vals)
     eps = w.eps()[:n_lanes]
     X, st, dt, cores = oracle_lanes(s, perm, eps, tol)
@@ -126,7 +126,7 @@ def run_reference(args):
     s = w.system()
     import oracle
     from oracle import ordering
-    perm = ordering.min_degree_order(s.n, s.row_ptr, s.col_idx)
+    perm = ordering.elimination_order(s.n, s.row_ptr, s.col_idx)
     tol = oracle.default_tol(s.n, s.row_ptr, s.col_idx, s.vals)
     lanes = args.ref_lanes
     eps_all = w.eps()

@@ -190,7 +190,7 @@ psp_status psp_synchronize(psp_handle h);
  * eps_out_h[2m] = [+s_1, -s_1, ..., +s_m, -s_m] and w_out_h[2m] = beta_j / 2 on both
  * signs, beta_j = prod_{l != j} s_l^2 / (s_l^2 - s_j^2) (the solution of
  * Gamma_m^T beta = e_1, computed in long double without forming Gamma).
- * Errors: ARG (m < 1, m > 64, repeated or zero magnitude). */
+ * Errors: ARG (m < 1, m > 256, repeated or zero magnitude). */
 psp_status psp_ladder_weights(int32_t m, const double* s_h, double* eps_out_h, double* w_out_h);
 
 #ifdef __cplusplus

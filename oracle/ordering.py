@@ -117,3 +117,54 @@ def permuted_csc(n, row_ptr, col_idx, vals, perm):
         vs += [v for _, v in c]
         colptr[j + 1] = colptr[j] + len(c)
     return colptr, np.array(rows, dtype=np.int32), np.array(vs, dtype=np.float64)
+
+
+def postorder_big_first(n, row_ptr, col_idx, perm0, first=None):
+    """Relabel an elimination order into a postorder of its elimination tree
+    (R13): the etree parent of column j is the smallest row index of
+    L(:, j) below the diagonal; each subtree gets the weight sum_{k in subtree}
+    |L(:, k)|^2; roots and the children of every node are visited by descending
+    weight, ties by ascending index; a node is emitted after its children.  If
+    `first` is given (the leading-zero regime) that vertex — a leaf, since it is
+    eliminated first — is moved to the front.  Returns perm[new] = old.  A
+    postorder is a topological order of the etree, so the filled pattern is the
+    same set of entries (relabelled)."""
+    fcp, fri = filled_pattern(n, row_ptr, col_idx, perm0)
+    lcount = [0] * n
+    parent = [-1] * n
+    for j in range(n):
+        rows = [int(r) for r in fri[fcp[j]:fcp[j + 1]] if r > j]
+        lcount[j] = len(rows)
+        parent[j] = min(rows) if rows else -1
+    weight = [lcount[j] ** 2 for j in range(n)]
+    for j in range(n):                      # children have smaller index than parents
+        if parent[j] >= 0:
+            weight[parent[j]] += weight[j]
+    children = [[] for _ in range(n)]
+    roots = []
+    for j in range(n):
+        (children[parent[j]] if parent[j] >= 0 else roots).append(j)
+    key = lambda v: (-weight[v], v)          # noqa: E731
+    order = []
+    stack = [(r, False) for r in sorted(roots, key=key, reverse=True)]
+    while stack:
+        v, done = stack.pop()
+        if done:
+            order.append(v)
+            continue
+        stack.append((v, True))
+        for c in sorted(children[v], key=key, reverse=True):
+            stack.append((c, False))
+    perm0 = np.asarray(perm0)
+    perm = [int(perm0[v]) for v in order]
+    if first is not None:
+        perm.remove(int(first))
+        perm.insert(0, int(first))
+    return np.array(perm, dtype=np.int32)
+
+
+def elimination_order(n, row_ptr, col_idx, first=None):
+    """The oracle's elimination order: exact minimum degree, then the big-first
+    postorder of its elimination tree (R13)."""
+    perm0 = min_degree_order(n, row_ptr, col_idx, first=first)
+    return postorder_big_first(n, row_ptr, col_idx, perm0, first=first)

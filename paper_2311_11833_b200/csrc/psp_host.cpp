@@ -17,6 +17,7 @@
 
 #include "../../include/psp.h"
 #include "psp_internal.h"
+#include "psp_plan.h"
 
 using psp::DevicePlan;
 using psp::kSlab;
@@ -44,10 +45,12 @@ struct psp_ctx {
   bool analysed = false;
   int32_t n = 0, nnz_A = 0, nnz_LU = 0, nnz_L = 0, n_levels = 0, n_struct_zero_diag = 0;
   int64_t factor_fma = 0, solve_fma = 0;
-  int32_t max_live = 0;
+  int32_t max_live = 0, y_slots = 0, x_slots = 0, c_max = 0;
   std::vector<int32_t> perm;
   std::vector<DevBuf> plan_bufs;
   DevicePlan plan;
+  psp::LaunchInfo launch;
+  DevBuf fscratch_d, sscratch_d;   // global pending buffers when shared memory is too small
 
   // --- perturbations ---
   int32_t K = 0, K_pad = 0;
@@ -119,93 +122,6 @@ static psp_status upload(psp_ctx* h, const std::vector<T>& v, const T** out) {
   return PSP_OK;
 }
 
-// ============================================================================
-// Ordering: exact minimum degree on the elimination graph (R13).
-// ============================================================================
-static std::vector<int32_t> min_degree(int32_t n, const std::vector<std::vector<int32_t>>& adj0,
-                                       int32_t first) {
-  std::vector<std::vector<int32_t>> adj = adj0;  // sorted neighbour lists
-  std::vector<char> alive(n, 1);
-  std::set<std::pair<int32_t, int32_t>> pq;      // (degree, vertex)
-  for (int32_t v = 0; v < n; ++v) pq.insert({(int32_t)adj[v].size(), v});
-  std::vector<int32_t> order;
-  order.reserve(n);
-  std::vector<int32_t> merged;
-  auto eliminate = [&](int32_t v) {
-    pq.erase({(int32_t)adj[v].size(), v});
-    alive[v] = 0;
-    order.push_back(v);
-    const std::vector<int32_t> nb = adj[v];
-    for (int32_t a : nb) {
-      pq.erase({(int32_t)adj[a].size(), a});
-      // adj[a] <- (adj[a] U nb) \ {a, v}
-      merged.clear();
-      std::set_union(adj[a].begin(), adj[a].end(), nb.begin(), nb.end(),
-                     std::back_inserter(merged));
-      merged.erase(std::remove_if(merged.begin(), merged.end(),
-                                  [&](int32_t x) { return x == a || x == v; }),
-                   merged.end());
-      adj[a].swap(merged);
-      pq.insert({(int32_t)adj[a].size(), a});
-    }
-    adj[v].clear();
-  };
-  if (first >= 0) eliminate(first);
-  while (!pq.empty()) eliminate(pq.begin()->second);
-  return order;
-}
-
-// ============================================================================
-// Symbolic factorisation via the elimination tree (Liu) and column merging.
-// ============================================================================
-struct SymbolicResult {
-  std::vector<std::vector<int32_t>> lcol;  // strictly-lower rows of each column (sorted)
-  std::vector<int32_t> parent, level;
-  int32_t height = 0;
-};
-
-static SymbolicResult symbolic_etree(int32_t n, const std::vector<std::vector<int32_t>>& adjp) {
-  // adjp: symmetric adjacency in the permuted numbering (no self loops), sorted.
-  SymbolicResult S;
-  S.parent.assign(n, -1);
-  std::vector<int32_t> anc(n, -1);
-  for (int32_t j = 0; j < n; ++j)
-    for (int32_t i : adjp[j]) {
-      if (i >= j) break;
-      int32_t r = i;
-      while (anc[r] != -1 && anc[r] != j) {
-        int32_t t = anc[r];
-        anc[r] = j;
-        r = t;
-      }
-      if (anc[r] == -1) {
-        anc[r] = j;
-        S.parent[r] = j;
-      }
-    }
-  std::vector<std::vector<int32_t>> children(n);
-  for (int32_t j = 0; j < n; ++j)
-    if (S.parent[j] >= 0) children[S.parent[j]].push_back(j);
-  S.lcol.assign(n, {});
-  S.level.assign(n, 0);
-  std::vector<int32_t> tmp;
-  for (int32_t j = 0; j < n; ++j) {
-    std::vector<int32_t>& L = S.lcol[j];
-    for (int32_t i : adjp[j])
-      if (i > j) L.push_back(i);
-    for (int32_t c : children[j]) {
-      tmp.clear();
-      std::set_union(L.begin(), L.end(), S.lcol[c].begin(), S.lcol[c].end(),
-                     std::back_inserter(tmp));
-      tmp.erase(std::remove(tmp.begin(), tmp.end(), j), tmp.end());
-      L.swap(tmp);
-      S.level[j] = std::max(S.level[j], S.level[c] + 1);
-    }
-    S.height = std::max(S.height, S.level[j] + 1);
-  }
-  return S;
-}
-
 static void release_plan(psp_ctx* h) {
   for (auto& b : h->plan_bufs) b.release();
   h->plan_bufs.clear();
@@ -218,6 +134,8 @@ static void reset_numeric(psp_ctx* h) {
   h->V_d.release();
   h->status_d.release();
   h->X_d.release();
+  h->fscratch_d.release();
+  h->sscratch_d.release();
   h->wptr_d.release();
   h->wlane_d.release();
   h->wval_d.release();
@@ -367,7 +285,22 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
   } else if (ordering == PSP_ORDER_USER) {
     perm.assign(user_perm_h, user_perm_h + n);
   } else {
-    perm = min_degree(n, adj, ordering == PSP_ORDER_MINDEG_FIRST ? first_node : -1);
+    const int32_t first = ordering == PSP_ORDER_MINDEG_FIRST ? first_node : -1;
+    std::vector<int32_t> perm0 = psp::min_degree_order(n, adj, first);
+    std::vector<int32_t> inv0(n);
+    for (int32_t i = 0; i < n; ++i) inv0[perm0[i]] = i;
+    std::vector<std::vector<int32_t>> adj0(n);
+    for (int32_t i = 0; i < n; ++i) {
+      for (int32_t j : adj[perm0[i]]) adj0[i].push_back(inv0[j]);
+      std::sort(adj0[i].begin(), adj0[i].end());
+    }
+    psp::EtreeResult S0 = psp::symbolic_etree(n, adj0);
+    std::vector<int32_t> post = psp::postorder_big_first(n, S0);
+    for (int32_t i = 0; i < n; ++i) perm[i] = perm0[post[i]];
+    if (first >= 0) {  // the forced-first vertex is an etree leaf: moving it to the front
+      perm.erase(std::find(perm.begin(), perm.end(), first));  // keeps a topological order
+      perm.insert(perm.begin(), first);
+    }
   }
   std::vector<int32_t> inv(n);
   for (int32_t i = 0; i < n; ++i) inv[perm[i]] = i;
@@ -377,75 +310,14 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
     for (int32_t j : adj[perm[i]]) adjp[i].push_back(inv[j]);
     std::sort(adjp[i].begin(), adjp[i].end());
   }
-  SymbolicResult S = symbolic_etree(n, adjp);
-
-  // U part of column j = { i < j : j in lcol(i) }
-  std::vector<std::vector<int32_t>> ucol(n);
-  for (int32_t i = 0; i < n; ++i)
-    for (int32_t j : S.lcol[i]) ucol[j].push_back(i);  // i ascending => sorted
-
-  // slot layout: column j = [ucol rows][diag][lcol rows]
-  std::vector<int32_t> colptr(n + 1, 0), diag_slot(n), col_end(n);
-  for (int32_t j = 0; j < n; ++j) {
-    diag_slot[j] = colptr[j] + (int32_t)ucol[j].size();
-    colptr[j + 1] = diag_slot[j] + 1 + (int32_t)S.lcol[j].size();
-    col_end[j] = colptr[j + 1];
-  }
-  const int64_t nnzLU64 = colptr[n];
+  psp::EtreeResult S = psp::symbolic_etree(n, adjp);
+  int64_t nnzLU64 = n;
+  for (int32_t j = 0; j < n; ++j) nnzLU64 += 2 * (int64_t)S.lcol[j].size();
   if (nnzLU64 > INT32_MAX / 2) return fail(h, PSP_ERR_ARG, "pattern too large");
-  const int32_t nnzLU = (int32_t)nnzLU64;
-  auto slot = [&](int32_t i, int32_t j) -> int32_t {
-    if (i == j) return diag_slot[j];
-    if (i < j) {
-      auto& u = ucol[j];
-      auto it = std::lower_bound(u.begin(), u.end(), i);
-      return colptr[j] + (int32_t)(it - u.begin());
-    }
-    auto& l = S.lcol[j];
-    auto it = std::lower_bound(l.begin(), l.end(), i);
-    return diag_slot[j] + 1 + (int32_t)(it - l.begin());
-  };
 
-  // A -> slot scatter map
-  std::vector<int32_t> a_src(nnzLU, -1);
-  for (int32_t r = 0; r < n; ++r)
-    for (int32_t q = row_ptr_h[r]; q < row_ptr_h[r + 1]; ++q)
-      a_src[slot(inv[r], inv[col_idx_h[q]])] = q;
-
-  // left-looking factor plan
-  std::vector<int32_t> col_gptr(n + 1, 0), g_u, g_ptr(1, 0), pr_l, pr_d;
-  for (int32_t j = 0; j < n; ++j) {
-    for (int32_t p : ucol[j]) {
-      g_u.push_back(slot(p, j));
-      for (int32_t i : S.lcol[p]) {
-        pr_l.push_back(slot(i, p));
-        pr_d.push_back(slot(i, j));
-      }
-      g_ptr.push_back((int32_t)pr_l.size());
-    }
-    col_gptr[j + 1] = (int32_t)g_u.size();
-  }
-
-  // row-oriented solve plans
-  std::vector<int32_t> rl_ptr(n + 1, 0), rl_slot, rl_col, ru_ptr(n + 1, 0), ru_slot, ru_col;
-  {
-    std::vector<std::vector<int32_t>> lrow(n);
-    for (int32_t j = 0; j < n; ++j)
-      for (int32_t i : S.lcol[j]) lrow[i].push_back(j);  // j ascending
-    for (int32_t i = 0; i < n; ++i) {
-      for (int32_t j : lrow[i]) {
-        rl_slot.push_back(slot(i, j));
-        rl_col.push_back(j);
-      }
-      rl_ptr[i + 1] = (int32_t)rl_slot.size();
-      // row i of U = { j > i : j in lcol(i) } (symmetric pattern), j descending
-      for (auto it = S.lcol[i].rbegin(); it != S.lcol[i].rend(); ++it) {
-        ru_slot.push_back(slot(i, *it));
-        ru_col.push_back(*it);
-      }
-      ru_ptr[i + 1] = (int32_t)ru_slot.size();
-    }
-  }
+  psp::HostPlan HP;
+  psp::build_programs(n, S.lcol, perm, row_ptr_h, col_idx_h, HP);
+  if (HP.f_slots + HP.c_max > 65535) return fail(h, PSP_ERR_UNSUPPORTED, "pending set too large");
 
   // CSC grouping of A's entries (original numbering) for the deterministic 1-norm
   std::vector<int32_t> acsc_ptr(n + 1, 0), acsc_q(nnzA);
@@ -457,61 +329,49 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
       for (int32_t q = row_ptr_h[r]; q < row_ptr_h[r + 1]; ++q) acsc_q[fillp[col_idx_h[q]]++] = q;
   }
 
-  // max simultaneously-live L values in postorder-free natural elimination order:
-  // L(:,p) is live from column p until the last column that reads it (max row).
-  {
-    std::vector<int32_t> delta(n + 1, 0);
-    for (int32_t p = 0; p < n; ++p)
-      if (!S.lcol[p].empty()) {
-        int32_t last = S.lcol[p].back();
-        delta[p] += (int32_t)S.lcol[p].size();
-        delta[last + 1] -= (int32_t)S.lcol[p].size();
-      }
-    int32_t cur = 0, mx = 0;
-    for (int32_t j = 0; j < n; ++j) {
-      cur += delta[j];
-      mx = std::max(mx, cur);
-    }
-    h->max_live = mx;
-  }
-
   DevicePlan P;
   P.n = n;
   P.nnz_A = nnzA;
-  P.nnz_LU = nnzLU;
+  P.nnz_LU = HP.nnz_LU;
+  P.c_max = HP.c_max;
+  P.f_slots = HP.f_slots;
+  P.y_slots = HP.y_slots;
+  P.x_slots = HP.x_slots;
   psp_status s;
 #define UP(vec, field) \
   if (!host_only && (s = upload(h, vec, &P.field))) return s;
-  UP(a_src, a_src);
-  UP(diag_slot, diag_slot);
-  UP(col_end, col_end);
-  UP(col_gptr, col_gptr);
-  UP(g_u, g_u);
-  UP(g_ptr, g_ptr);
-  UP(pr_l, pr_l);
-  UP(pr_d, pr_d);
-  UP(rl_ptr, rl_ptr);
-  UP(rl_slot, rl_slot);
-  UP(rl_col, rl_col);
-  UP(ru_ptr, ru_ptr);
-  UP(ru_slot, ru_slot);
-  UP(ru_col, ru_col);
+  UP(HP.blk, blk);
   UP(perm, perm);
+  UP(HP.f_ptr, f_ptr);
+  UP(HP.f_code, f_code);
+  UP(HP.f_upd_ptr, f_upd_ptr);
+  UP(HP.y_ptr, y_ptr);
+  UP(HP.y_code, y_code);
+  UP(HP.x_ptr, x_ptr);
+  UP(HP.x_code, x_code);
   UP(acsc_ptr, acsc_ptr);
   UP(acsc_q, acsc_q);
 #undef UP
+  if (!host_only) {
+    const uint16_t* up16 = nullptr;
+    if ((s = upload(h, HP.f_upd, &up16))) return s;
+    P.f_upd = reinterpret_cast<const int4*>(up16);
+    CUDA_TRY(h, psp::configure_kernels(P, h->launch));
+  }
   h->plan = P;
   h->perm = perm;
   h->n = n;
   h->nnz_A = nnzA;
-  h->nnz_LU = nnzLU;
-  int32_t nnzL = 0;
-  for (int32_t j = 0; j < n; ++j) nnzL += (int32_t)S.lcol[j].size();
-  h->nnz_L = nnzL;
+  h->nnz_LU = HP.nnz_LU;
+  h->nnz_L = HP.nnz_L;
   h->n_levels = S.height;
   h->n_struct_zero_diag = nzd;
-  h->factor_fma = (int64_t)pr_l.size();
-  h->solve_fma = (int64_t)rl_slot.size() + (int64_t)ru_slot.size();
+  h->factor_fma = HP.factor_fma;
+  h->solve_fma = HP.solve_fma;
+  h->max_live = HP.f_slots;
+  h->y_slots = HP.y_slots;
+  h->x_slots = HP.x_slots;
+  h->c_max = HP.c_max;
   h->analysed = true;
   return PSP_OK;
 }
@@ -529,7 +389,8 @@ psp_status psp_get_symbolic_info(psp_handle h, psp_symbolic_info* info, int32_t*
   info->factor_div = h->nnz_L;
   info->solve_fma = h->solve_fma;
   info->max_live = h->max_live;
-  info->kernel_variant = 0;
+  // 1 = pending buffer in shared memory, 2 = global scratch (psp_kernels.cu)
+  info->kernel_variant = (h->max_live + h->c_max) * psp::kSlab * 8 <= 57 * 1024 ? 1 : 2;
   if (perm_h) std::copy(h->perm.begin(), h->perm.end(), perm_h);
   return PSP_OK;
 }
@@ -574,10 +435,18 @@ psp_status psp_factor_batch(psp_handle h, const double* A_vals, double pivot_tol
     CUDA_TRY(h, psp::launch_pivot_tol(h->plan, A_vals, (double*)h->tol_d.p, h->stream));
     tol_dev = (const double*)h->tol_d.p;
   }
-  CUDA_TRY(h, psp::launch_factor(h->plan, A_vals, (const double*)h->eps_d.p,
+  if (h->launch.factor_smem_bytes == 0) {
+    psp_status s;
+    size_t need = sizeof(double) * (size_t)h->K_pad * (h->plan.f_slots + h->plan.c_max);
+    if (h->fscratch_d.bytes < need) {
+      CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+      if ((s = ensure(h, h->fscratch_d, need))) return s;
+    }
+  }
+  CUDA_TRY(h, psp::launch_factor(h->plan, h->launch, A_vals, (const double*)h->eps_d.p,
                                  (const double*)h->dperm_d.p, tol_dev, pivot_tol,
-                                 (double*)h->V_d.p, (int32_t*)h->status_d.p, h->K, h->K_pad,
-                                 h->stream));
+                                 (double*)h->V_d.p, (double*)h->fscratch_d.p,
+                                 (int32_t*)h->status_d.p, h->K_pad, h->stream));
   if (lane_status)
     CUDA_TRY(h, cudaMemcpyAsync(lane_status, h->status_d.p, sizeof(int32_t) * h->K,
                                 cudaMemcpyDeviceToDevice, h->stream));
@@ -597,8 +466,15 @@ psp_status psp_solve_batch(psp_handle h, int32_t R, const double* B, int64_t ldb
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     if ((s = ensure(h, h->X_d, need))) return s;
   }
-  CUDA_TRY(h, psp::launch_solve(h->plan, (const double*)h->V_d.p, B, ldb, R, (double*)h->X_d.p,
-                                h->K_pad, h->stream));
+  if (h->launch.solve_smem_bytes == 0) {
+    size_t need2 = sizeof(double) * (size_t)h->K_pad * (h->plan.y_slots + h->plan.x_slots);
+    if (h->sscratch_d.bytes < need2) {
+      CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+      if ((s = ensure(h, h->sscratch_d, need2))) return s;
+    }
+  }
+  CUDA_TRY(h, psp::launch_solve(h->plan, h->launch, (const double*)h->V_d.p, B, ldb, R,
+                                (double*)h->X_d.p, (double*)h->sscratch_d.p, h->K_pad, h->stream));
   h->R = R;
   h->solved = true;
   return PSP_OK;
@@ -700,7 +576,7 @@ psp_status psp_solve_host(psp_handle h, const double* A_vals_h, int32_t R, const
 }
 
 psp_status psp_ladder_weights(int32_t m, const double* s_h, double* eps_out_h, double* w_out_h) {
-  if (m < 1 || m > 64 || !s_h || !eps_out_h || !w_out_h) return PSP_ERR_ARG;
+  if (m < 1 || m > 256 || !s_h || !eps_out_h || !w_out_h) return PSP_ERR_ARG;
   for (int32_t j = 0; j < m; ++j) {
     if (!(s_h[j] != 0.0) || !std::isfinite(s_h[j])) return PSP_ERR_ARG;
     for (int32_t l = 0; l < j; ++l)

@@ -1,0 +1,334 @@
+// Symbolic planning (host, once per sparsity pattern): elimination order, filled
+// pattern, pivot-major slot layout, and the interpreted "programs" the CUDA kernels
+// walk.  SURVEY §8(a) row a0; PAPER P:L82 (a static pivot sequence "computed once,
+// and perpetually reused").
+//
+// Elimination order (R13): exact minimum degree on the elimination graph
+// of pattern(A + A^T) (ties to the lowest original index), then the postorder of its
+// elimination tree with the heaviest subtree first.  A postorder is a topological
+// order of the etree, so the fill is unchanged; it keeps the set of partially
+// updated ("pending") entries small, which is what lets a lane's working set live
+// in shared memory.
+//
+// Factor program (right-looking, canonical order): pivot p (ascending) reads its
+// final pivot, L column and U row, writes them to the lane's output block
+// [u_pp][l_{i_0 p} .. l_{i_{c-1} p}][u_{p i_0} .. u_{p i_{c-1}}] (i_k = rows of L(:,p),
+// ascending), then applies a_ij = fma(-l_ip, u_pj, a_ij) to the c x c block
+// {i_a} x {i_b}.  Every entry therefore receives its updates in ascending pivot
+// order, exactly as in the dense Gaussian elimination of the oracle.  Entries that
+// have been updated but are not yet final live in numbered "pending slots"; an
+// entry is born (initialised from A, plus eps*d on the diagonal) right before its
+// first update and dies when its pivot consumes it.  Slots are reused greedily
+// (interval colouring), so the slot count equals the peak pending set.
+#include "psp_plan.h"
+
+#include <algorithm>
+#include <climits>
+#include <functional>
+#include <set>
+
+namespace psp {
+
+std::vector<int32_t> min_degree_order(int32_t n, const std::vector<std::vector<int32_t>>& adj0,
+                                      int32_t first) {
+  std::vector<std::vector<int32_t>> adj = adj0;  // sorted neighbour lists
+  std::set<std::pair<int32_t, int32_t>> pq;      // (degree, vertex)
+  for (int32_t v = 0; v < n; ++v) pq.insert({(int32_t)adj[v].size(), v});
+  std::vector<int32_t> order;
+  order.reserve(n);
+  std::vector<int32_t> merged;
+  auto eliminate = [&](int32_t v) {
+    pq.erase({(int32_t)adj[v].size(), v});
+    order.push_back(v);
+    const std::vector<int32_t> nb = adj[v];
+    for (int32_t a : nb) {
+      pq.erase({(int32_t)adj[a].size(), a});
+      merged.clear();
+      std::set_union(adj[a].begin(), adj[a].end(), nb.begin(), nb.end(),
+                     std::back_inserter(merged));
+      merged.erase(std::remove_if(merged.begin(), merged.end(),
+                                  [&](int32_t x) { return x == a || x == v; }),
+                   merged.end());
+      adj[a].swap(merged);
+      pq.insert({(int32_t)adj[a].size(), a});
+    }
+    adj[v].clear();
+  };
+  if (first >= 0) eliminate(first);
+  while (!pq.empty()) eliminate(pq.begin()->second);
+  return order;
+}
+
+EtreeResult symbolic_etree(int32_t n, const std::vector<std::vector<int32_t>>& adjp) {
+  EtreeResult S;
+  S.parent.assign(n, -1);
+  std::vector<int32_t> anc(n, -1);
+  for (int32_t j = 0; j < n; ++j)
+    for (int32_t i : adjp[j]) {
+      if (i >= j) break;
+      int32_t r = i;
+      while (anc[r] != -1 && anc[r] != j) {
+        int32_t t = anc[r];
+        anc[r] = j;
+        r = t;
+      }
+      if (anc[r] == -1) {
+        anc[r] = j;
+        S.parent[r] = j;
+      }
+    }
+  std::vector<std::vector<int32_t>> children(n);
+  for (int32_t j = 0; j < n; ++j)
+    if (S.parent[j] >= 0) children[S.parent[j]].push_back(j);
+  S.lcol.assign(n, {});
+  S.level.assign(n, 0);
+  std::vector<int32_t> tmp;
+  for (int32_t j = 0; j < n; ++j) {
+    std::vector<int32_t>& L = S.lcol[j];
+    for (int32_t i : adjp[j])
+      if (i > j) L.push_back(i);
+    for (int32_t c : children[j]) {
+      tmp.clear();
+      std::set_union(L.begin(), L.end(), S.lcol[c].begin(), S.lcol[c].end(),
+                     std::back_inserter(tmp));
+      tmp.erase(std::remove(tmp.begin(), tmp.end(), j), tmp.end());
+      L.swap(tmp);
+      S.level[j] = std::max(S.level[j], S.level[c] + 1);
+    }
+    S.height = std::max(S.height, S.level[j] + 1);
+  }
+  return S;
+}
+
+// Heaviest-subtree-first postorder of the etree given by parent[] (children have
+// smaller indices).  weight(j) = sum over the subtree of |L(:,k)|^2.
+std::vector<int32_t> postorder_big_first(int32_t n, const EtreeResult& S) {
+  std::vector<int64_t> w(n);
+  for (int32_t j = 0; j < n; ++j) w[j] = (int64_t)S.lcol[j].size() * (int64_t)S.lcol[j].size();
+  for (int32_t j = 0; j < n; ++j)
+    if (S.parent[j] >= 0) w[S.parent[j]] += w[j];
+  std::vector<std::vector<int32_t>> children(n);
+  std::vector<int32_t> roots;
+  for (int32_t j = 0; j < n; ++j) (S.parent[j] >= 0 ? children[S.parent[j]] : roots).push_back(j);
+  auto before = [&](int32_t a, int32_t b) { return w[a] != w[b] ? w[a] > w[b] : a < b; };
+  std::sort(roots.begin(), roots.end(), before);
+  for (auto& c : children) std::sort(c.begin(), c.end(), before);
+  std::vector<int32_t> order;
+  order.reserve(n);
+  // iterative DFS: (node, next child index)
+  std::vector<std::pair<int32_t, size_t>> st;
+  for (int32_t r : roots) {
+    st.push_back({r, 0});
+    while (!st.empty()) {
+      auto& top = st.back();
+      if (top.second < children[top.first].size()) {
+        int32_t c = children[top.first][top.second++];
+        st.push_back({c, 0});
+      } else {
+        order.push_back(top.first);
+        st.pop_back();
+      }
+    }
+  }
+  return order;
+}
+
+namespace {
+
+// Greedy interval colouring: items with [birth, death] in step order; returns the
+// slot of each item and the number of slots.  `release_same_step` = a slot whose
+// item dies at step s may be reused by an item born at step s.
+int32_t colour(int32_t n_steps, const std::vector<int32_t>& birth, const std::vector<int32_t>& death,
+               bool release_same_step, std::vector<int32_t>& slot) {
+  const int32_t m = (int32_t)birth.size();
+  std::vector<std::vector<int32_t>> born(n_steps + 1), dies(n_steps + 1);
+  for (int32_t e = 0; e < m; ++e) {
+    if (birth[e] < 0) continue;
+    born[birth[e]].push_back(e);
+    dies[death[e]].push_back(e);
+  }
+  slot.assign(m, -1);
+  std::vector<int32_t> free_list;
+  int32_t used = 0;
+  for (int32_t s = 0; s < n_steps; ++s) {
+    if (release_same_step)
+      for (int32_t e : dies[s]) free_list.push_back(slot[e]);
+    for (int32_t e : born[s]) {
+      if (!free_list.empty()) {
+        slot[e] = free_list.back();
+        free_list.pop_back();
+      } else {
+        slot[e] = used++;
+      }
+    }
+    if (!release_same_step)
+      for (int32_t e : dies[s]) free_list.push_back(slot[e]);
+  }
+  return used;
+}
+
+}  // namespace
+
+void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
+                    const std::vector<int32_t>& perm, const int32_t* row_ptr_h,
+                    const int32_t* col_idx_h, HostPlan& P) {
+  P.n = n;
+  P.perm = perm;
+  P.blk.assign(n + 1, 0);
+  P.c_max = 0;
+  int64_t nnzL = 0, ffma = 0;
+  for (int32_t p = 0; p < n; ++p) {
+    const int32_t c = (int32_t)lcol[p].size();
+    P.blk[p + 1] = P.blk[p] + 1 + 2 * c;
+    P.c_max = std::max(P.c_max, c);
+    nnzL += c;
+    ffma += (int64_t)c * c;
+  }
+  P.nnz_LU = P.blk[n];
+  P.nnz_L = (int32_t)nnzL;
+  P.factor_fma = ffma;
+  P.solve_fma = 2 * nnzL;
+
+  // A lookup in the permuted numbering: (i, j) -> CSR index of A(perm[i], perm[j]) or -1
+  auto a_index = [&](int32_t i, int32_t j) -> int32_t {
+    const int32_t r = perm[i], c = perm[j];
+    const int32_t* b = col_idx_h + row_ptr_h[r];
+    const int32_t* e = col_idx_h + row_ptr_h[r + 1];
+    const int32_t* it = std::lower_bound(b, e, c);
+    return (it != e && *it == c) ? (int32_t)(it - col_idx_h) : -1;
+  };
+  // entry ids: diag p -> p; L(i,j) (i>j) -> n + off[j] + pos; U(i,j) (i<j) -> n + nnzL + off[i] + pos
+  std::vector<int32_t> off(n + 1, 0);
+  for (int32_t p = 0; p < n; ++p) off[p + 1] = off[p] + (int32_t)lcol[p].size();
+  const int32_t n_ent = n + 2 * (int32_t)nnzL;
+  auto pos_in = [&](int32_t col, int32_t row) -> int32_t {
+    const auto& v = lcol[col];
+    return (int32_t)(std::lower_bound(v.begin(), v.end(), row) - v.begin());
+  };
+  auto entry = [&](int32_t i, int32_t j) -> int32_t {
+    if (i == j) return i;
+    if (i > j) return n + off[j] + pos_in(j, i);
+    return n + (int32_t)nnzL + off[i] + pos_in(i, j);
+  };
+
+  // ---------------- factor ----------------
+  std::vector<int32_t> first(n_ent, -1), death(n_ent, -1);
+  for (int32_t p = 0; p < n; ++p) {
+    const auto& L = lcol[p];
+    for (int32_t a : L)
+      for (int32_t b : L) {
+        const int32_t e = entry(a, b);
+        if (first[e] < 0) {
+          first[e] = p;
+          death[e] = std::min(a, b);
+        }
+      }
+  }
+  std::vector<int32_t> fslot;
+  P.f_slots = colour(n, first, death, false, fslot);
+  P.f_births = 0;
+  P.f_ptr.assign(n + 1, 0);
+  P.f_code.clear();
+  P.f_upd_ptr.assign(n + 1, 0);
+  P.f_upd.clear();
+  std::vector<std::vector<int32_t>> births_at(n);
+  for (int32_t e = 0; e < n_ent; ++e)
+    if (first[e] >= 0) births_at[first[e]].push_back(e);
+  // inverse entry -> (i, j) for births
+  std::vector<int32_t> ent_i(n_ent), ent_j(n_ent);
+  for (int32_t p = 0; p < n; ++p) {
+    ent_i[p] = ent_j[p] = p;
+    for (size_t k = 0; k < lcol[p].size(); ++k) {
+      const int32_t i = lcol[p][k];
+      ent_i[n + off[p] + k] = i;  // L(i, p)
+      ent_j[n + off[p] + k] = p;
+      ent_i[n + nnzL + off[p] + k] = p;  // U(p, i)
+      ent_j[n + nnzL + off[p] + k] = i;
+    }
+  }
+  auto src_code = [&](int32_t i, int32_t j) -> int32_t {
+    const int32_t e = entry(i, j);
+    if (first[e] >= 0) return fslot[e];
+    const int32_t q = a_index(i, j);
+    return q >= 0 ? -1 - q : INT_MIN;
+  };
+  for (int32_t p = 0; p < n; ++p) {
+    const auto& L = lcol[p];
+    const int32_t c = (int32_t)L.size();
+    auto& fc = P.f_code;
+    fc.push_back((int32_t)births_at[p].size());
+    fc.push_back(c);
+    fc.push_back(src_code(p, p));
+    for (int32_t e : births_at[p]) {
+      const int32_t i = ent_i[e], j = ent_j[e];
+      fc.push_back(fslot[e]);
+      fc.push_back(a_index(i, j));
+      fc.push_back(i == j ? i : -1);
+      ++P.f_births;
+    }
+    for (int32_t k = 0; k < c; ++k) fc.push_back(src_code(L[k], p));
+    for (int32_t k = 0; k < c; ++k) fc.push_back(src_code(p, L[k]));
+    P.f_ptr[p + 1] = (int32_t)fc.size();
+    // update slots: chunk-major, 8 uint16 per row-chunk
+    for (int32_t jc = 0; jc * 8 < c; ++jc)
+      for (int32_t a = 0; a < c; ++a)
+        for (int32_t b = 0; b < 8; ++b) {
+          const int32_t col = jc * 8 + b;
+          P.f_upd.push_back(col < c ? (uint16_t)fslot[entry(L[a], L[col])] : (uint16_t)0);
+        }
+    P.f_upd_ptr[p + 1] = (int32_t)(P.f_upd.size() / 8);
+  }
+
+  // ---------------- forward substitution (column-oriented, ascending) ----------
+  {
+    std::vector<int32_t> yb(n, -1), yd(n, -1);
+    for (int32_t j = 0; j < n; ++j)
+      for (int32_t i : lcol[j])
+        if (yb[i] < 0) {
+          yb[i] = j;
+          yd[i] = i;
+        }
+    std::vector<int32_t> ys;
+    P.y_slots = colour(n, yb, yd, false, ys);
+    std::vector<std::vector<int32_t>> yborn(n);
+    for (int32_t i = 0; i < n; ++i)
+      if (yb[i] >= 0) yborn[yb[i]].push_back(i);
+    P.y_ptr.assign(n + 1, 0);
+    P.y_code.clear();
+    for (int32_t j = 0; j < n; ++j) {
+      auto& yc = P.y_code;
+      yc.push_back((int32_t)yborn[j].size());
+      yc.push_back((int32_t)lcol[j].size());
+      yc.push_back(yb[j] >= 0 ? ys[j] : -1);
+      for (int32_t i : yborn[j]) {
+        yc.push_back(ys[i]);
+        yc.push_back(perm[i]);
+      }
+      for (int32_t i : lcol[j]) yc.push_back(ys[i]);
+      P.y_ptr[j + 1] = (int32_t)yc.size();
+    }
+  }
+  // ---------------- backward substitution (row-oriented, descending) ----------
+  {
+    // step s = n-1-i; x_i born at step of i, dies at the step of the smallest q with i in lcol(q)
+    std::vector<int32_t> xb(n, -1), xd(n, -1);
+    for (int32_t q = 0; q < n; ++q)
+      for (int32_t i : lcol[q])
+        if (xd[i] < 0 || n - 1 - q > xd[i]) xd[i] = n - 1 - q;
+    for (int32_t i = 0; i < n; ++i)
+      if (xd[i] >= 0) xb[i] = n - 1 - i;
+    std::vector<int32_t> xs;
+    P.x_slots = colour(n, xb, xd, true, xs);
+    P.x_ptr.assign(n + 1, 0);
+    P.x_code.clear();
+    for (int32_t i = 0; i < n; ++i) {
+      auto& xc = P.x_code;
+      xc.push_back((int32_t)lcol[i].size());
+      xc.push_back(xb[i] >= 0 ? xs[i] : -1);
+      for (int32_t k : lcol[i]) xc.push_back(xs[k]);
+      P.x_ptr[i + 1] = (int32_t)xc.size();
+    }
+  }
+}
+
+}  // namespace psp

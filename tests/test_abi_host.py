@@ -62,7 +62,7 @@ def test_ordering_and_fill_parity_with_oracle(ci, first):
     info, perm = hs.analyse(s.n, s.row_ptr, s.col_idx,
                             ordering="mindeg_first" if first else "mindeg",
                             first_node=-1 if f is None else f)
-    operm = ordering.min_degree_order(s.n, s.row_ptr, s.col_idx, first=f)
+    operm = ordering.elimination_order(s.n, s.row_ptr, s.col_idx, first=f)
     assert np.array_equal(perm, operm)                      # integer parity, bit-exact
     fcp, fri = ordering.filled_pattern(s.n, s.row_ptr, s.col_idx, perm)
     assert info["nnz_LU"] == int(fcp[-1])

@@ -28,7 +28,7 @@ def gpu_run(s, eps, ordering_kind="mindeg", first=-1, tol=0.0, B=None, ladders=N
     if ordering_kind == "natural":
         operm = np.arange(s.n, dtype=np.int32)
     else:
-        operm = ordering.min_degree_order(s.n, s.row_ptr, s.col_idx, first=None if first < 0 else first)
+        operm = ordering.elimination_order(s.n, s.row_ptr, s.col_idx, first=None if first < 0 else first)
     assert np.array_equal(perm, operm)
     solver.psp_set_perturbations(eps, s.d)
     A = torch.tensor(s.vals, dtype=torch.float64, device="cuda")
@@ -51,7 +51,7 @@ def gpu_run(s, eps, ordering_kind="mindeg", first=-1, tol=0.0, B=None, ladders=N
 
 
 def oracle_perm(s, first):
-    return ordering.min_degree_order(s.n, s.row_ptr, s.col_idx, first=None if first < 0 else first)
+    return ordering.elimination_order(s.n, s.row_ptr, s.col_idx, first=None if first < 0 else first)
 
 
 def rel(a, b):

@@ -208,7 +208,7 @@ def test_combination_affine_invariance():
 def test_300bus_recovery_and_residual(first):
     w = config(1)
     s = w.system()
-    perm = ordering.min_degree_order(s.n, s.row_ptr, s.col_idx, first=s.slot_p if first else None)
+    perm = ordering.elimination_order(s.n, s.row_ptr, s.col_idx, first=s.slot_p if first else None)
     tol = oracle.default_tol(s.n, s.row_ptr, s.col_idx, s.vals)
     xh, X, st = pipeline(s, perm, w.ladders, tol)
     assert (st == 0).all()

@@ -141,7 +141,7 @@ def test_or2_equals_or1_bitwise():
         w = config(ci)
         s = w.system()
         for first in [None, s.slot_p]:
-            perm = ordering.min_degree_order(s.n, s.row_ptr, s.col_idx, first=first)
+            perm = ordering.elimination_order(s.n, s.row_ptr, s.col_idx, first=first)
             tol = oracle.default_tol(s.n, s.row_ptr, s.col_idx, s.vals)
             eps = np.r_[w.eps(), 1e-6, -1e-8]
             X1, st1 = oracle.dense_batch(s, perm, eps, tol)
@@ -155,7 +155,7 @@ def test_leading_zero_fails_unperturbed_and_succeeds_perturbed():
     # "A leading 0 was always encountered on a diagonal" -> pivot-free fails;
     # the perturbed lanes (Alg. 1) succeed.
     s = config(1).system()
-    perm = ordering.min_degree_order(s.n, s.row_ptr, s.col_idx, first=s.slot_p)
+    perm = ordering.elimination_order(s.n, s.row_ptr, s.col_idx, first=s.slot_p)
     assert perm[0] == s.slot_p
     tol = oracle.default_tol(s.n, s.row_ptr, s.col_idx, s.vals)
     X, st = oracle.SparseOracle(s, perm).batch(np.array([0.0, 2e-3, -2e-3]), tol)
@@ -254,3 +254,21 @@ def test_filled_pattern_equals_numeric_structure():
     for j in range(n):
         sym[fri[fcp[j]:fcp[j + 1]], j] = True
     assert np.array_equal(sym, LU != 0)
+
+
+@pytest.mark.parametrize("ci", [0, 1, 3])
+def test_postorder_is_topological_and_keeps_fill(ci):
+    s = config(ci).system()
+    p0 = ordering.min_degree_order(s.n, s.row_ptr, s.col_idx)
+    p1 = ordering.postorder_big_first(s.n, s.row_ptr, s.col_idx, p0)
+    assert sorted(p1.tolist()) == list(range(s.n))
+    f0 = ordering.filled_pattern(s.n, s.row_ptr, s.col_idx, p0)
+    f1 = ordering.filled_pattern(s.n, s.row_ptr, s.col_idx, p1)
+    assert f0[0][-1] == f1[0][-1]
+    # etree parent of every column comes after it (postorder is topological)
+    fcp, fri = f1
+    for j in range(s.n):
+        rows = fri[fcp[j]:fcp[j + 1]]
+        below = rows[rows > j]
+        if len(below):
+            assert below.min() > j
