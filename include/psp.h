@@ -78,8 +78,13 @@ typedef struct {
   int64_t factor_fma;            /* fused multiply-adds per lane in the factorisation */
   int64_t factor_div;            /* divisions per lane (strictly-lower slots)        */
   int64_t solve_fma;             /* fmas per lane per right-hand side (fwd + bwd)    */
-  int32_t max_live;              /* max simultaneously-live L values per lane (plan) */
-  int32_t kernel_variant;        /* factor kernel chosen by the plan  */
+  int32_t max_live;              /* pending slots per lane: peak number of partially-
+                                    updated entries of the right-looking factorisation */
+  int32_t kernel_variant;        /* 1: pending slots + A in shared memory, 2: pending in
+                                    shared memory, A in global, 3: pending in global
+                                    scratch                            */
+  int32_t solve_live;            /* live slots per lane of the triangular solves     */
+  int32_t births;                /* pending-slot initialisations per lane            */
 } psp_symbolic_info;
 
 /* ---- lifetime ---------------------------------------------------------------- */

@@ -45,7 +45,7 @@ struct psp_ctx {
   bool analysed = false;
   int32_t n = 0, nnz_A = 0, nnz_LU = 0, nnz_L = 0, n_levels = 0, n_struct_zero_diag = 0;
   int64_t factor_fma = 0, solve_fma = 0;
-  int32_t max_live = 0, y_slots = 0, x_slots = 0, c_max = 0;
+  int32_t max_live = 0, y_slots = 0, x_slots = 0, c_max = 0, f_births = 0;
   std::vector<int32_t> perm;
   std::vector<DevBuf> plan_bufs;
   DevicePlan plan;
@@ -333,31 +333,31 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
   P.n = n;
   P.nnz_A = nnzA;
   P.nnz_LU = HP.nnz_LU;
+  P.nnz_L = HP.nnz_L;
   P.c_max = HP.c_max;
   P.f_slots = HP.f_slots;
+  P.f_chunk_words = HP.f_chunk_words;
+  P.f_nchunks = (int32_t)(HP.f_stream.size() / HP.f_chunk_words);
   P.y_slots = HP.y_slots;
+  P.y_chunk_words = HP.y_chunk_words;
+  P.y_nchunks = (int32_t)(HP.y_stream.size() / HP.y_chunk_words);
   P.x_slots = HP.x_slots;
+  P.x_chunk_words = HP.x_chunk_words;
+  P.x_nchunks = (int32_t)(HP.x_stream.size() / HP.x_chunk_words);
   psp_status s;
 #define UP(vec, field) \
   if (!host_only && (s = upload(h, vec, &P.field))) return s;
-  UP(HP.blk, blk);
   UP(perm, perm);
-  UP(HP.f_ptr, f_ptr);
-  UP(HP.f_code, f_code);
-  UP(HP.f_upd_ptr, f_upd_ptr);
-  UP(HP.y_ptr, y_ptr);
-  UP(HP.y_code, y_code);
-  UP(HP.x_ptr, x_ptr);
-  UP(HP.x_code, x_code);
+  UP(HP.f_stream, f_stream);
+  UP(HP.y_stream, y_stream);
+  UP(HP.x_stream, x_stream);
   UP(acsc_ptr, acsc_ptr);
   UP(acsc_q, acsc_q);
 #undef UP
-  if (!host_only) {
-    const uint16_t* up16 = nullptr;
-    if ((s = upload(h, HP.f_upd, &up16))) return s;
-    P.f_upd = reinterpret_cast<const int4*>(up16);
+  if (host_only)
+    psp::choose_launch(P, h->launch);
+  else
     CUDA_TRY(h, psp::configure_kernels(P, h->launch));
-  }
   h->plan = P;
   h->perm = perm;
   h->n = n;
@@ -372,6 +372,7 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
   h->y_slots = HP.y_slots;
   h->x_slots = HP.x_slots;
   h->c_max = HP.c_max;
+  h->f_births = HP.f_births;
   h->analysed = true;
   return PSP_OK;
 }
@@ -389,8 +390,9 @@ psp_status psp_get_symbolic_info(psp_handle h, psp_symbolic_info* info, int32_t*
   info->factor_div = h->nnz_L;
   info->solve_fma = h->solve_fma;
   info->max_live = h->max_live;
-  // 1 = pending buffer in shared memory, 2 = global scratch (psp_kernels.cu)
-  info->kernel_variant = (h->max_live + h->c_max) * psp::kSlab * 8 <= 57 * 1024 ? 1 : 2;
+  info->kernel_variant = h->launch.f_pend_smem ? (h->launch.f_a_smem ? 1 : 2) : 3;
+  info->solve_live = h->y_slots + h->x_slots;
+  info->births = h->f_births;
   if (perm_h) std::copy(h->perm.begin(), h->perm.end(), perm_h);
   return PSP_OK;
 }
@@ -435,7 +437,7 @@ psp_status psp_factor_batch(psp_handle h, const double* A_vals, double pivot_tol
     CUDA_TRY(h, psp::launch_pivot_tol(h->plan, A_vals, (double*)h->tol_d.p, h->stream));
     tol_dev = (const double*)h->tol_d.p;
   }
-  if (h->launch.factor_smem_bytes == 0) {
+  if (!h->launch.f_pend_smem) {
     psp_status s;
     size_t need = sizeof(double) * (size_t)h->K_pad * (h->plan.f_slots + h->plan.c_max);
     if (h->fscratch_d.bytes < need) {
@@ -466,7 +468,7 @@ psp_status psp_solve_batch(psp_handle h, int32_t R, const double* B, int64_t ldb
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     if ((s = ensure(h, h->X_d, need))) return s;
   }
-  if (h->launch.solve_smem_bytes == 0) {
+  if (!h->launch.s_live_smem) {
     size_t need2 = sizeof(double) * (size_t)h->K_pad * (h->plan.y_slots + h->plan.x_slots);
     if (h->sscratch_d.bytes < need2) {
       CUDA_TRY(h, cudaStreamSynchronize(h->stream));

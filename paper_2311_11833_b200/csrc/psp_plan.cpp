@@ -167,6 +167,26 @@ int32_t colour(int32_t n_steps, const std::vector<int32_t>& birth, const std::ve
   return used;
 }
 
+// Pack 16-byte-aligned records into fixed-size chunks (the kernels stream chunks
+// into shared-memory rings with bulk async copies).  A record never straddles a
+// chunk; the rest of a chunk after its last record starts with the sentinel -1.
+void pack_chunks(const std::vector<std::vector<int32_t>>& recs, size_t max_rec,
+                 int32_t& chunk_words, std::vector<int32_t>& out) {
+  chunk_words = 256;  // 1 KB
+  while ((size_t)chunk_words < max_rec + 4) chunk_words *= 2;
+  out.assign(chunk_words, -1);
+  size_t base = 0, used = 0;
+  for (const auto& r : recs) {
+    if (used + r.size() + 4 > (size_t)chunk_words) {
+      base += chunk_words;
+      used = 0;
+      out.resize(base + chunk_words, -1);
+    }
+    std::copy(r.begin(), r.end(), out.begin() + base + used);
+    used += r.size();
+  }
+}
+
 }  // namespace
 
 void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
@@ -174,17 +194,19 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
                     const int32_t* col_idx_h, HostPlan& P) {
   P.n = n;
   P.perm = perm;
-  P.blk.assign(n + 1, 0);
+  P.lofs.assign(n + 1, 0);
+  P.dofs.assign(n + 1, 0);
   P.c_max = 0;
   int64_t nnzL = 0, ffma = 0;
   for (int32_t p = 0; p < n; ++p) {
     const int32_t c = (int32_t)lcol[p].size();
-    P.blk[p + 1] = P.blk[p] + 1 + 2 * c;
+    P.lofs[p + 1] = P.lofs[p] + c;
+    P.dofs[p + 1] = P.dofs[p] + 1 + c;
     P.c_max = std::max(P.c_max, c);
     nnzL += c;
     ffma += (int64_t)c * c;
   }
-  P.nnz_LU = P.blk[n];
+  P.nnz_LU = P.lofs[n] + P.dofs[n];
   P.nnz_L = (int32_t)nnzL;
   P.factor_fma = ffma;
   P.solve_fma = 2 * nnzL;
@@ -227,13 +249,6 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
   std::vector<int32_t> fslot;
   P.f_slots = colour(n, first, death, false, fslot);
   P.f_births = 0;
-  P.f_ptr.assign(n + 1, 0);
-  P.f_code.clear();
-  P.f_upd_ptr.assign(n + 1, 0);
-  P.f_upd.clear();
-  std::vector<std::vector<int32_t>> births_at(n);
-  for (int32_t e = 0; e < n_ent; ++e)
-    if (first[e] >= 0) births_at[first[e]].push_back(e);
   // inverse entry -> (i, j) for births
   std::vector<int32_t> ent_i(n_ent), ent_j(n_ent);
   for (int32_t p = 0; p < n; ++p) {
@@ -246,39 +261,47 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
       ent_j[n + nnzL + off[p] + k] = i;
     }
   }
+  std::vector<std::vector<int32_t>> births_at(n);
+  for (int32_t e = 0; e < n_ent; ++e)
+    if (first[e] >= 0) births_at[first[e]].push_back(e);
   auto src_code = [&](int32_t i, int32_t j) -> int32_t {
     const int32_t e = entry(i, j);
     if (first[e] >= 0) return fslot[e];
     const int32_t q = a_index(i, j);
     return q >= 0 ? -1 - q : INT_MIN;
   };
+  // Factor stream: one record per pivot (16-byte aligned), packed into fixed-size
+  // chunks that the kernel pulls into a shared-memory ring with bulk async copies.
+  std::vector<std::vector<int32_t>> recs(n);
+  size_t max_rec = 0;
+  P.f_births = 0;
   for (int32_t p = 0; p < n; ++p) {
     const auto& L = lcol[p];
     const int32_t c = (int32_t)L.size();
-    auto& fc = P.f_code;
-    fc.push_back((int32_t)births_at[p].size());
-    fc.push_back(c);
-    fc.push_back(src_code(p, p));
+    const int32_t nb = (int32_t)births_at[p].size();
+    std::vector<int32_t>& r = recs[p];
+    r = {c | (nb << 16), src_code(p, p), P.lofs[p], P.dofs[p]};
     for (int32_t e : births_at[p]) {
       const int32_t i = ent_i[e], j = ent_j[e];
-      fc.push_back(fslot[e]);
-      fc.push_back(a_index(i, j));
-      fc.push_back(i == j ? i : -1);
+      r.push_back(fslot[e]);
+      r.push_back(a_index(i, j));
+      r.push_back(i == j ? i : -1);
       ++P.f_births;
     }
-    for (int32_t k = 0; k < c; ++k) fc.push_back(src_code(L[k], p));
-    for (int32_t k = 0; k < c; ++k) fc.push_back(src_code(p, L[k]));
-    P.f_ptr[p + 1] = (int32_t)fc.size();
-    // update slots: chunk-major, 8 uint16 per row-chunk
+    for (int32_t k = 0; k < c; ++k) r.push_back(src_code(L[k], p));
+    for (int32_t k = 0; k < c; ++k) r.push_back(src_code(p, L[k]));
+    while (r.size() % 4) r.push_back(0);
     for (int32_t jc = 0; jc * 8 < c; ++jc)
       for (int32_t a = 0; a < c; ++a)
-        for (int32_t b = 0; b < 8; ++b) {
-          const int32_t col = jc * 8 + b;
-          P.f_upd.push_back(col < c ? (uint16_t)fslot[entry(L[a], L[col])] : (uint16_t)0);
+        for (int32_t b = 0; b < 8; b += 2) {
+          const int32_t c0 = jc * 8 + b, c1 = c0 + 1;
+          const uint32_t s0 = c0 < c ? (uint32_t)fslot[entry(L[a], L[c0])] : 0u;
+          const uint32_t s1 = c1 < c ? (uint32_t)fslot[entry(L[a], L[c1])] : 0u;
+          r.push_back((int32_t)(s0 | (s1 << 16)));
         }
-    P.f_upd_ptr[p + 1] = (int32_t)(P.f_upd.size() / 8);
+    max_rec = std::max(max_rec, r.size());
   }
-
+  pack_chunks(recs, max_rec, P.f_chunk_words, P.f_stream);
   // ---------------- forward substitution (column-oriented, ascending) ----------
   {
     std::vector<int32_t> yb(n, -1), yd(n, -1);
@@ -293,20 +316,21 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
     std::vector<std::vector<int32_t>> yborn(n);
     for (int32_t i = 0; i < n; ++i)
       if (yb[i] >= 0) yborn[yb[i]].push_back(i);
-    P.y_ptr.assign(n + 1, 0);
-    P.y_code.clear();
+    std::vector<std::vector<int32_t>> yrec(n);
+    size_t ymax = 0;
     for (int32_t j = 0; j < n; ++j) {
-      auto& yc = P.y_code;
-      yc.push_back((int32_t)yborn[j].size());
-      yc.push_back((int32_t)lcol[j].size());
-      yc.push_back(yb[j] >= 0 ? ys[j] : -1);
+      auto& yc = yrec[j];
+      yc = {(int32_t)lcol[j].size() | ((int32_t)yborn[j].size() << 16), yb[j] >= 0 ? ys[j] : -1,
+            P.lofs[j], 0};
       for (int32_t i : yborn[j]) {
         yc.push_back(ys[i]);
         yc.push_back(perm[i]);
       }
       for (int32_t i : lcol[j]) yc.push_back(ys[i]);
-      P.y_ptr[j + 1] = (int32_t)yc.size();
+      while (yc.size() % 4) yc.push_back(0);
+      ymax = std::max(ymax, yc.size());
     }
+    pack_chunks(yrec, ymax, P.y_chunk_words, P.y_stream);
   }
   // ---------------- backward substitution (row-oriented, descending) ----------
   {
@@ -319,15 +343,17 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
       if (xd[i] >= 0) xb[i] = n - 1 - i;
     std::vector<int32_t> xs;
     P.x_slots = colour(n, xb, xd, true, xs);
-    P.x_ptr.assign(n + 1, 0);
-    P.x_code.clear();
-    for (int32_t i = 0; i < n; ++i) {
-      auto& xc = P.x_code;
-      xc.push_back((int32_t)lcol[i].size());
-      xc.push_back(xb[i] >= 0 ? xs[i] : -1);
+    // records in processing order (pivots descending)
+    std::vector<std::vector<int32_t>> xrec;
+    size_t xmax = 0;
+    for (int32_t i = n - 1; i >= 0; --i) {
+      std::vector<int32_t> xc = {(int32_t)lcol[i].size(), xb[i] >= 0 ? xs[i] : -1, P.dofs[i], i};
       for (int32_t k : lcol[i]) xc.push_back(xs[k]);
-      P.x_ptr[i + 1] = (int32_t)xc.size();
+      while (xc.size() % 4) xc.push_back(0);
+      xmax = std::max(xmax, xc.size());
+      xrec.push_back(std::move(xc));
     }
+    pack_chunks(xrec, xmax, P.x_chunk_words, P.x_stream);
   }
 }
 

@@ -16,14 +16,14 @@ struct HostPlan {
   int32_t n = 0, nnz_LU = 0, nnz_L = 0, c_max = 0;
   int64_t factor_fma = 0, solve_fma = 0;
   std::vector<int32_t> perm;   // perm[new] = old
-  std::vector<int32_t> blk;    // [n+1] pivot block offsets: [u_pp][L col][U row]
-  // factor
-  int32_t f_slots = 0, f_births = 0;
-  std::vector<int32_t> f_ptr, f_code, f_upd_ptr;
-  std::vector<uint16_t> f_upd;
-  // forward / backward substitution
-  int32_t y_slots = 0, x_slots = 0;
-  std::vector<int32_t> y_ptr, y_code, x_ptr, x_code;
+  // per-lane factor layout: L region (column p of L at lofs[p], c_p values) followed
+  // by the DU region (u_pp then U row p at nnz_L + dofs[p], 1 + c_p values)
+  std::vector<int32_t> lofs, dofs;  // [n+1]
+  // factor / forward / backward programs: record streams packed in chunks
+  int32_t f_slots = 0, f_births = 0, f_chunk_words = 0;
+  std::vector<int32_t> f_stream;
+  int32_t y_slots = 0, x_slots = 0, y_chunk_words = 0, x_chunk_words = 0;
+  std::vector<int32_t> y_stream, x_stream;
 };
 
 std::vector<int32_t> min_degree_order(int32_t n, const std::vector<std::vector<int32_t>>& adj,

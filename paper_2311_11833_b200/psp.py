@@ -32,7 +32,8 @@ class SymbolicInfo(ctypes.Structure):
                 ("nnz_L", ctypes.c_int32), ("n_struct_zero_diag", ctypes.c_int32),
                 ("n_levels", ctypes.c_int32), ("factor_fma", ctypes.c_int64),
                 ("factor_div", ctypes.c_int64), ("solve_fma", ctypes.c_int64),
-                ("max_live", ctypes.c_int32), ("kernel_variant", ctypes.c_int32)]
+                ("max_live", ctypes.c_int32), ("kernel_variant", ctypes.c_int32),
+                ("solve_live", ctypes.c_int32), ("births", ctypes.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
