@@ -439,7 +439,7 @@ psp_status psp_factor_batch(psp_handle h, const double* A_vals, double pivot_tol
   }
   if (!h->launch.f_pend_smem) {
     psp_status s;
-    size_t need = sizeof(double) * (size_t)h->K_pad * (h->plan.f_slots + h->plan.c_max);
+    size_t need = sizeof(double) * (size_t)h->K_pad * (h->plan.f_slots + 2 * h->plan.c_max);
     if (h->fscratch_d.bytes < need) {
       CUDA_TRY(h, cudaStreamSynchronize(h->stream));
       if ((s = ensure(h, h->fscratch_d, need))) return s;

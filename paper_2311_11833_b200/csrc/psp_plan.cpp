@@ -270,37 +270,60 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
     const int32_t q = a_index(i, j);
     return q >= 0 ? -1 - q : INT_MIN;
   };
-  // Factor stream: one record per pivot (16-byte aligned), packed into fixed-size
-  // chunks that the kernel pulls into a shared-memory ring with bulk async copies.
-  std::vector<std::vector<int32_t>> recs(n);
+  // Factor stream (records 16-byte aligned, packed into fixed-size chunks that the
+  // kernel pulls into a shared-memory ring with bulk async copies):
+  //   BIRTH  [1<<28 | nb, 0, 0, 0] + nb x (slot, A index or -1, d index or -1), nb <= 64
+  //   PIVOT  [2<<28 | c, pivot source, lofs, dofs] + c L sources + c U sources
+  //   UPDATE [3<<28 | j0, a0, na, w] + na int4 rows of 8 uint16 target slots:
+  //          rows a0..a0+na-1, columns j0..j0+w-1 of the pivot's c x c block
+  //   END    [4<<28, 0, 0, 0]
+  std::vector<std::vector<int32_t>> recs;
   size_t max_rec = 0;
   P.f_births = 0;
+  auto push = [&](std::vector<int32_t>&& r) {
+    while (r.size() % 4) r.push_back(0);
+    max_rec = std::max(max_rec, r.size());
+    recs.push_back(std::move(r));
+  };
   for (int32_t p = 0; p < n; ++p) {
     const auto& L = lcol[p];
     const int32_t c = (int32_t)L.size();
-    const int32_t nb = (int32_t)births_at[p].size();
-    std::vector<int32_t>& r = recs[p];
-    r = {c | (nb << 16), src_code(p, p), P.lofs[p], P.dofs[p]};
-    for (int32_t e : births_at[p]) {
-      const int32_t i = ent_i[e], j = ent_j[e];
-      r.push_back(fslot[e]);
-      r.push_back(a_index(i, j));
-      r.push_back(i == j ? i : -1);
-      ++P.f_births;
+    const auto& bl = births_at[p];
+    for (size_t b0 = 0; b0 < bl.size(); b0 += 64) {
+      const size_t b1 = std::min(bl.size(), b0 + 64);
+      std::vector<int32_t> r = {(int32_t)((1u << 28) | (uint32_t)(b1 - b0)), 0, 0, 0};
+      for (size_t q = b0; q < b1; ++q) {
+        const int32_t e = bl[q], i = ent_i[e], j = ent_j[e];
+        r.push_back(fslot[e]);
+        r.push_back(a_index(i, j));
+        r.push_back(i == j ? i : -1);
+        ++P.f_births;
+      }
+      push(std::move(r));
     }
-    for (int32_t k = 0; k < c; ++k) r.push_back(src_code(L[k], p));
-    for (int32_t k = 0; k < c; ++k) r.push_back(src_code(p, L[k]));
-    while (r.size() % 4) r.push_back(0);
-    for (int32_t jc = 0; jc * 8 < c; ++jc)
-      for (int32_t a = 0; a < c; ++a)
-        for (int32_t b = 0; b < 8; b += 2) {
-          const int32_t c0 = jc * 8 + b, c1 = c0 + 1;
-          const uint32_t s0 = c0 < c ? (uint32_t)fslot[entry(L[a], L[c0])] : 0u;
-          const uint32_t s1 = c1 < c ? (uint32_t)fslot[entry(L[a], L[c1])] : 0u;
-          r.push_back((int32_t)(s0 | (s1 << 16)));
-        }
-    max_rec = std::max(max_rec, r.size());
+    {
+      std::vector<int32_t> r = {(int32_t)((2u << 28) | (uint32_t)c), src_code(p, p), P.lofs[p], P.dofs[p]};
+      for (int32_t k = 0; k < c; ++k) r.push_back(src_code(L[k], p));
+      for (int32_t k = 0; k < c; ++k) r.push_back(src_code(p, L[k]));
+      push(std::move(r));
+    }
+    for (int32_t j0 = 0; j0 < c; j0 += 8) {
+      const int32_t wdt = std::min(8, c - j0);
+      for (int32_t a0 = 0; a0 < c; a0 += 32) {
+        const int32_t na = std::min(32, c - a0);
+        std::vector<int32_t> r = {(int32_t)((3u << 28) | (uint32_t)j0), a0, na, wdt};
+        for (int32_t a = a0; a < a0 + na; ++a)
+          for (int32_t b = 0; b < 8; b += 2) {
+            const int32_t c0 = j0 + b, c1 = c0 + 1;
+            const uint32_t s0 = b < wdt ? (uint32_t)fslot[entry(L[a], L[c0])] : 0u;
+            const uint32_t s1 = b + 1 < wdt ? (uint32_t)fslot[entry(L[a], L[c1])] : 0u;
+            r.push_back((int32_t)(s0 | (s1 << 16)));
+          }
+        push(std::move(r));
+      }
+    }
   }
+  push({(int32_t)(4u << 28), 0, 0, 0});
   pack_chunks(recs, max_rec, P.f_chunk_words, P.f_stream);
   // ---------------- forward substitution (column-oriented, ascending) ----------
   {
@@ -316,20 +339,32 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
     std::vector<std::vector<int32_t>> yborn(n);
     for (int32_t i = 0; i < n; ++i)
       if (yb[i] >= 0) yborn[yb[i]].push_back(i);
-    std::vector<std::vector<int32_t>> yrec(n);
+    std::vector<std::vector<int32_t>> yrec;
     size_t ymax = 0;
+    auto ypush = [&](std::vector<int32_t>&& r) {
+      while (r.size() % 4) r.push_back(0);
+      ymax = std::max(ymax, r.size());
+      yrec.push_back(std::move(r));
+    };
+    // YBIRTH [1<<28 | nb, 0, 0, 0] + nb x (slot, original row);  YPIVOT [2<<28 | c, ys, lofs, 0]
+    // + c target slots;  END [4<<28, ...]
     for (int32_t j = 0; j < n; ++j) {
-      auto& yc = yrec[j];
-      yc = {(int32_t)lcol[j].size() | ((int32_t)yborn[j].size() << 16), yb[j] >= 0 ? ys[j] : -1,
-            P.lofs[j], 0};
-      for (int32_t i : yborn[j]) {
-        yc.push_back(ys[i]);
-        yc.push_back(perm[i]);
+      const auto& bl = yborn[j];
+      for (size_t b0 = 0; b0 < bl.size(); b0 += 64) {
+        const size_t b1 = std::min(bl.size(), b0 + 64);
+        std::vector<int32_t> r = {(int32_t)((1u << 28) | (uint32_t)(b1 - b0)), 0, 0, 0};
+        for (size_t q = b0; q < b1; ++q) {
+          r.push_back(ys[bl[q]]);
+          r.push_back(perm[bl[q]]);
+        }
+        ypush(std::move(r));
       }
-      for (int32_t i : lcol[j]) yc.push_back(ys[i]);
-      while (yc.size() % 4) yc.push_back(0);
-      ymax = std::max(ymax, yc.size());
+      std::vector<int32_t> r = {(int32_t)((2u << 28) | (uint32_t)lcol[j].size()),
+                                yb[j] >= 0 ? ys[j] : -1, P.lofs[j], 0};
+      for (int32_t i : lcol[j]) r.push_back(ys[i]);
+      ypush(std::move(r));
     }
+    ypush({(int32_t)(4u << 28), 0, 0, 0});
     pack_chunks(yrec, ymax, P.y_chunk_words, P.y_stream);
   }
   // ---------------- backward substitution (row-oriented, descending) ----------
