@@ -80,8 +80,9 @@ typedef struct {
   int64_t solve_fma;             /* fmas per lane per right-hand side (fwd + bwd)    */
   int32_t max_live;              /* pending slots per lane: peak number of partially-
                                     updated entries of the right-looking factorisation */
-  int32_t kernel_variant;        /* 1: pending slots + A in shared memory, 2: pending in
-                                    shared memory, A in global, 3: pending in global
+  int32_t kernel_variant;        /* 0: pattern-specialised generated kernels; interpreter
+                                    with 1: pending slots + A in shared memory, 2: pending
+                                    in shared memory, A in global, 3: pending in global
                                     scratch                            */
   int32_t solve_live;            /* live slots per lane of the triangular solves     */
   int32_t births;                /* pending-slot initialisations per lane            */
@@ -98,6 +99,22 @@ psp_status psp_create(psp_handle* out, int32_t device, void* cuda_stream);
 
 /* Release all device and host memory of the handle (synchronises its stream). */
 psp_status psp_destroy(psp_handle h);
+
+/* Options (set before psp_symbolic_analyse; they apply to the next analysis):
+ *  PSP_OPT_CODEGEN          0: interpreter kernels only; 1: use a pattern-specialised
+ *                           kernel only if it is already in the on-disk cache; 2 (default):
+ *                           generate, compile (nvJitLink, sm_100a) and cache it when absent.
+ *                           The cache directory is $PSP_KERNEL_CACHE or <dir of libpsp.so>/kcache.
+ *  PSP_OPT_CODEGEN_MAX_FMA  largest factor fma count per lane for which kernels are
+ *                           generated (default 40000; compile time grows with it).
+ *  PSP_OPT_MAX_REGS         register cap of the generated kernels (0 = ptxas default).
+ * Generated and interpreted kernels are bitwise identical (same canonical order).
+ * Errors: ARG. */
+enum { PSP_OPT_CODEGEN = 1, PSP_OPT_CODEGEN_MAX_FMA = 2, PSP_OPT_MAX_REGS = 3 };
+psp_status psp_set_option(psp_handle h, int32_t option, int64_t value);
+
+/* Human-readable state of the pattern-specialised kernels after psp_symbolic_analyse. */
+const char* psp_codegen_status(psp_handle h);
 
 /* Rebind the handle to another stream of the same device. */
 psp_status psp_set_stream(psp_handle h, void* cuda_stream);

@@ -59,10 +59,10 @@ cudaError_t launch_pivot_tol(const DevicePlan& p, const double* A_vals, double* 
 cudaError_t launch_factor(const DevicePlan& p, const LaunchInfo& li, const double* A_vals,
                           const double* eps, const double* dperm, const double* tol_dev,
                           double tol_value, double* V, double* gscratch, int32_t* status,
-                          int32_t K_pad, cudaStream_t stream);
+                          int32_t K_pad, const int32_t* only, cudaStream_t stream);
 cudaError_t launch_solve(const DevicePlan& p, const LaunchInfo& li, const double* V,
                          const double* B, int64_t ldb, int32_t R, double* X, double* gscratch,
-                         int32_t K_pad, cudaStream_t stream);
+                         int32_t K_pad, const int32_t* only, cudaStream_t stream);
 cudaError_t launch_recover(const DevicePlan& p, int32_t W, int32_t R, const int32_t* w_ptr,
                            const int32_t* w_lane, const double* w_val, const double* X,
                            const int32_t* status, double* x_out, int32_t* infeasible_flag,

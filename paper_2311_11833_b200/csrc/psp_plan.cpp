@@ -276,10 +276,12 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
   //   PIVOT  [2<<28 | c, pivot source, lofs, dofs] + c L sources + c U sources
   //   UPDATE [3<<28 | j0, a0, na, w] + na int4 rows of 8 uint16 target slots:
   //          rows a0..a0+na-1, columns j0..j0+w-1 of the pivot's c x c block
+  //   UPDATE32 [5<<28 | j0, a0, na, w] + na x 8 int32 slots (pending sets >= 65536)
   //   END    [4<<28, 0, 0, 0]
   std::vector<std::vector<int32_t>> recs;
   size_t max_rec = 0;
   P.f_births = 0;
+  const bool wide = P.f_slots + 2 * P.c_max > 65535;
   auto push = [&](std::vector<int32_t>&& r) {
     while (r.size() % 4) r.push_back(0);
     max_rec = std::max(max_rec, r.size());
@@ -311,14 +313,20 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
       const int32_t wdt = std::min(8, c - j0);
       for (int32_t a0 = 0; a0 < c; a0 += 32) {
         const int32_t na = std::min(32, c - a0);
-        std::vector<int32_t> r = {(int32_t)((3u << 28) | (uint32_t)j0), a0, na, wdt};
-        for (int32_t a = a0; a < a0 + na; ++a)
+        std::vector<int32_t> r = {(int32_t)(((wide ? 5u : 3u) << 28) | (uint32_t)j0), a0, na, wdt};
+        for (int32_t a = a0; a < a0 + na; ++a) {
+          if (wide) {  // 8 int32 slots per row (two int4)
+            for (int32_t b = 0; b < 8; ++b)
+              r.push_back(b < wdt ? fslot[entry(L[a], L[j0 + b])] : 0);
+            continue;
+          }
           for (int32_t b = 0; b < 8; b += 2) {
             const int32_t c0 = j0 + b, c1 = c0 + 1;
             const uint32_t s0 = b < wdt ? (uint32_t)fslot[entry(L[a], L[c0])] : 0u;
             const uint32_t s1 = b + 1 < wdt ? (uint32_t)fslot[entry(L[a], L[c1])] : 0u;
             r.push_back((int32_t)(s0 | (s1 << 16)));
           }
+        }
         push(std::move(r));
       }
     }

@@ -24,7 +24,8 @@ EXPORTS = ["psp_create", "psp_destroy", "psp_set_stream", "psp_status_string",
            "psp_last_error_detail", "psp_symbolic_analyse", "psp_get_symbolic_info",
            "psp_set_perturbations", "psp_factor_batch", "psp_solve_batch", "psp_get_solutions",
            "psp_set_weights", "psp_recover", "psp_get_lane_status", "psp_solve_host",
-           "psp_synchronize", "psp_ladder_weights"]
+           "psp_synchronize", "psp_ladder_weights", "psp_set_option", "psp_codegen_status"]
+OPT = {"codegen": 1, "codegen_max_fma": 2, "max_regs": 3}
 
 
 class SymbolicInfo(ctypes.Structure):
@@ -72,6 +73,7 @@ def lib():
             "psp_get_lane_status": [P, P],
             "psp_solve_host": [P, P, I32, P, D, P],
             "psp_ladder_weights": [I32, P, P, P],
+            "psp_set_option": [P, I32, I64],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -81,6 +83,8 @@ def lib():
         L.psp_status_string.restype = ctypes.c_char_p
         L.psp_last_error_detail.argtypes = [P]
         L.psp_last_error_detail.restype = ctypes.c_char_p
+        L.psp_codegen_status.argtypes = [P]
+        L.psp_codegen_status.restype = ctypes.c_char_p
         _lib = L
     return _lib
 
@@ -134,6 +138,12 @@ class Solver:
     __del__ = close
 
     # --- C-ABI wrappers ------------------------------------------------------
+    def psp_set_option(self, name, value):
+        self._check(lib().psp_set_option(self.h, OPT[name], int(value)))
+
+    def psp_codegen_status(self):
+        return lib().psp_codegen_status(self.h).decode()
+
     def psp_symbolic_analyse(self, n, row_ptr, col_idx, ordering="mindeg", user_perm=None, first_node=-1):
         rp = np.ascontiguousarray(row_ptr, dtype=np.int32)
         ci = np.ascontiguousarray(col_idx, dtype=np.int32)
@@ -245,6 +255,14 @@ class HostSymbolic:
         if st:
             raise PSPError(st, "psp_create(host-only)")
         self.h = h
+
+    def set_option(self, name, value):
+        st = lib().psp_set_option(self.h, OPT[name], int(value))
+        if st:
+            raise PSPError(st, lib().psp_last_error_detail(self.h).decode())
+
+    def codegen_status(self):
+        return lib().psp_codegen_status(self.h).decode()
 
     def analyse(self, n, row_ptr, col_idx, ordering="mindeg", user_perm=None, first_node=-1):
         rp = np.ascontiguousarray(row_ptr, dtype=np.int32)
