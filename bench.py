@@ -169,6 +169,8 @@ def main():
     ap.add_argument("--cpu-lanes", type=int, default=512, help="oracle sample for cpu_baseline")
     ap.add_argument("--ref-lanes", type=int, default=256, help="oracle lanes per reference step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--groups", type=int, default=0, help="PSP_OPT_FACTOR_GROUPS (0 = auto)")
+    ap.add_argument("--warps", type=int, default=0, help="PSP_OPT_FACTOR_WARPS (0 = auto)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -192,6 +194,8 @@ def main():
     K = len(eps)
     stream = torch.cuda.current_stream()
     solver = psp.Solver(local_rank, stream)
+    solver.psp_set_option("factor_groups", args.groups)
+    solver.psp_set_option("factor_warps", args.warps)
     t0 = time.perf_counter()
     solver.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering="mindeg")
     t_sym = time.perf_counter() - t0

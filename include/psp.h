@@ -80,12 +80,13 @@ typedef struct {
   int64_t solve_fma;             /* fmas per lane per right-hand side (fwd + bwd)    */
   int32_t max_live;              /* pending slots per lane: peak number of partially-
                                     updated entries of the right-looking factorisation */
-  int32_t kernel_variant;        /* 0: pattern-specialised generated kernels; interpreter
-                                    with 1: pending slots + A in shared memory, 2: pending
-                                    in shared memory, A in global, 3: pending in global
-                                    scratch                            */
   int32_t solve_live;            /* live slots per lane of the triangular solves     */
   int32_t births;                /* pending-slot initialisations per lane            */
+  int32_t factor_groups;         /* G: thread groups sharing one slab of 32/G lanes in
+                                    the factor kernel                 */
+  int32_t factor_warps_per_cta;  /* consumer warps per factor CTA                    */
+  int32_t factor_pend_smem;      /* 1: pending slots in shared memory, 0: global     */
+  int32_t solve_live_smem;       /* 1: solve's live slots in shared memory, 0: global */
 } psp_symbolic_info;
 
 /* ---- lifetime ---------------------------------------------------------------- */
@@ -101,20 +102,14 @@ psp_status psp_create(psp_handle* out, int32_t device, void* cuda_stream);
 psp_status psp_destroy(psp_handle h);
 
 /* Options (set before psp_symbolic_analyse; they apply to the next analysis):
- *  PSP_OPT_CODEGEN          0: interpreter kernels only; 1: use a pattern-specialised
- *                           kernel only if it is already in the on-disk cache; 2 (default):
- *                           generate, compile (nvJitLink, sm_100a) and cache it when absent.
- *                           The cache directory is $PSP_KERNEL_CACHE or <dir of libpsp.so>/kcache.
- *  PSP_OPT_CODEGEN_MAX_FMA  largest factor fma count per lane for which kernels are
- *                           generated (default 40000; compile time grows with it).
- *  PSP_OPT_MAX_REGS         register cap of the generated kernels (0 = ptxas default).
- * Generated and interpreted kernels are bitwise identical (same canonical order).
+ *  PSP_OPT_FACTOR_GROUPS  0 (default): automatic; else G in {1, 2, 4, 8}: the factor
+ *                         kernel splits each warp into G groups sharing one slab of
+ *                         32/G lanes.  Results are bitwise independent of G.
+ *  PSP_OPT_FACTOR_WARPS   0 (default): automatic; else consumer warps per factor CTA
+ *                         (1..16, capped by shared memory).
  * Errors: ARG. */
-enum { PSP_OPT_CODEGEN = 1, PSP_OPT_CODEGEN_MAX_FMA = 2, PSP_OPT_MAX_REGS = 3 };
+enum { PSP_OPT_FACTOR_GROUPS = 1, PSP_OPT_FACTOR_WARPS = 2 };
 psp_status psp_set_option(psp_handle h, int32_t option, int64_t value);
-
-/* Human-readable state of the pattern-specialised kernels after psp_symbolic_analyse. */
-const char* psp_codegen_status(psp_handle h);
 
 /* Rebind the handle to another stream of the same device. */
 psp_status psp_set_stream(psp_handle h, void* cuda_stream);
@@ -174,6 +169,13 @@ psp_status psp_solve_batch(psp_handle h, int32_t R, const double* B, int64_t ldb
 /* Copy the per-lane solutions to X (device, K x R x n, lane-major, ORIGINAL
  * ordering): X[(k*R + r)*n + i] = x_k,r[i].  Errors: ARG, STATE. */
 psp_status psp_get_solutions(psp_handle h, double* X);
+
+/* Copy lane k's factor to the host (synchronises the stream): vals_h[nnz_LU] in the
+ * pivot-major layout of the permuted matrix: first the L region (for p = 0..n-1: l_{i p}
+ * for the rows i of L(:, p) ascending), then the DU region (for p = 0..n-1: u_pp, then
+ * u_{p i} for the same i).  The row sets are those of the symbolic factorisation of
+ * pattern(A + A^T + I) in the order of psp_get_symbolic_info's perm.  Errors: ARG, STATE. */
+psp_status psp_get_factor(psp_handle h, int32_t k, double* vals_h);
 
 /* Recombination weights (Remark 2 / Eq. (13), with the pair average of
  * Eq. (avg_hats), folded in: weight beta_j / 2 on each sign).  CSR over

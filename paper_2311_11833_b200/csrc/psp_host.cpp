@@ -18,10 +18,9 @@
 #include "../../include/psp.h"
 #include "psp_internal.h"
 #include "psp_plan.h"
-#include "psp_codegen.h"
 
 using psp::DevicePlan;
-using psp::kSlab;
+using psp::kBlock;
 
 namespace {
 
@@ -51,12 +50,7 @@ struct psp_ctx {
   std::vector<DevBuf> plan_bufs;
   DevicePlan plan;
   psp::LaunchInfo launch;
-  // pattern-specialised kernels (kernel_variant 0)
-  psp::GenKernels gen;
-  bool gen_ok = false;
-  std::string gen_msg;
-  int64_t opt_codegen = 2, opt_codegen_max_fma = 40000, opt_max_regs = 0;
-  DevBuf flags_d;
+  int64_t opt_groups = 0, opt_warps = 0;   // PSP_OPT_FACTOR_GROUPS / _WARPS (0 = automatic)
   DevBuf fscratch_d, sscratch_d;   // global pending buffers when shared memory is too small
 
   // --- perturbations ---
@@ -130,8 +124,6 @@ static psp_status upload(psp_ctx* h, const std::vector<T>& v, const T** out) {
 }
 
 static void release_plan(psp_ctx* h) {
-  psp::release_gen_kernels(h->gen);
-  h->gen_ok = false;
   for (auto& b : h->plan_bufs) b.release();
   h->plan_bufs.clear();
   h->plan = DevicePlan{};
@@ -143,7 +135,6 @@ static void reset_numeric(psp_ctx* h) {
   h->V_d.release();
   h->status_d.release();
   h->X_d.release();
-  h->flags_d.release();
   h->fscratch_d.release();
   h->sscratch_d.release();
   h->wptr_d.release();
@@ -219,27 +210,19 @@ psp_status psp_destroy(psp_handle h) {
 psp_status psp_set_option(psp_handle h, int32_t option, int64_t value) {
   if (!h) return PSP_ERR_ARG;
   switch (option) {
-    case PSP_OPT_CODEGEN:
-      if (value < 0 || value > 2) return fail(h, PSP_ERR_ARG, "PSP_OPT_CODEGEN must be 0, 1 or 2");
-      h->opt_codegen = value;
+    case PSP_OPT_FACTOR_GROUPS:
+      if (value != 0 && value != 1 && value != 2 && value != 4 && value != 8)
+        return fail(h, PSP_ERR_ARG, "PSP_OPT_FACTOR_GROUPS must be 0, 1, 2, 4 or 8");
+      h->opt_groups = value;
       return PSP_OK;
-    case PSP_OPT_CODEGEN_MAX_FMA:
-      if (value < 0) return fail(h, PSP_ERR_ARG, "negative limit");
-      h->opt_codegen_max_fma = value;
-      return PSP_OK;
-    case PSP_OPT_MAX_REGS:
-      if (value != 0 && (value < 32 || value > 255)) return fail(h, PSP_ERR_ARG, "registers in [32, 255]");
-      h->opt_max_regs = value;
+    case PSP_OPT_FACTOR_WARPS:
+      if (value < 0 || value > psp::kMaxWarpsCta)
+        return fail(h, PSP_ERR_ARG, "PSP_OPT_FACTOR_WARPS must be in [0, %d]", psp::kMaxWarpsCta);
+      h->opt_warps = value;
       return PSP_OK;
     default:
       return fail(h, PSP_ERR_ARG, "unknown option %d", option);
   }
-}
-
-const char* psp_codegen_status(psp_handle h) {
-  if (!h) return "null handle";
-  if (h->gen_ok) return h->gen.from_cache ? "generated kernels loaded from cache" : "generated kernels compiled";
-  return h->gen_msg.empty() ? "code generation off" : h->gen_msg.c_str();
 }
 
 psp_status psp_set_stream(psp_handle h, void* cuda_stream) {
@@ -374,49 +357,23 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
   P.f_chunk_words = HP.f_chunk_words;
   P.f_nchunks = (int32_t)(HP.f_stream.size() / HP.f_chunk_words);
   P.y_slots = HP.y_slots;
-  P.y_chunk_words = HP.y_chunk_words;
-  P.y_nchunks = (int32_t)(HP.y_stream.size() / HP.y_chunk_words);
   P.x_slots = HP.x_slots;
-  P.x_chunk_words = HP.x_chunk_words;
-  P.x_nchunks = (int32_t)(HP.x_stream.size() / HP.x_chunk_words);
+  P.s_chunk_words = HP.s_chunk_words;
+  P.s_nchunks = (int32_t)(HP.s_stream.size() / HP.s_chunk_words);
   psp_status s;
 #define UP(vec, field) \
   if (!host_only && (s = upload(h, vec, &P.field))) return s;
   UP(perm, perm);
+  UP(HP.adiag, adiag);
   UP(HP.f_stream, f_stream);
-  UP(HP.y_stream, y_stream);
-  UP(HP.x_stream, x_stream);
+  UP(HP.s_stream, s_stream);
   UP(acsc_ptr, acsc_ptr);
   UP(acsc_q, acsc_q);
 #undef UP
   if (host_only)
-    psp::choose_launch(P, h->launch);
+    psp::choose_launch(P, h->launch, (int)h->opt_groups, (int)h->opt_warps);
   else
-    CUDA_TRY(h, psp::configure_kernels(P, h->launch));
-  h->gen_msg.clear();
-  if (h->opt_codegen > 0 && HP.factor_fma <= h->opt_codegen_max_fma) {
-    psp::GenInput gi;
-    gi.n = n;
-    gi.nnz_L = HP.nnz_L;
-    gi.nnz_LU = HP.nnz_LU;
-    gi.lcol = &S.lcol;
-    gi.perm = &perm;
-    gi.lofs = &HP.lofs;
-    gi.dofs = &HP.dofs;
-    gi.max_regs = (int)h->opt_max_regs;
-    gi.a_index = [&](int32_t i, int32_t j) -> int32_t {
-      const int32_t r = perm[i], c = perm[j];
-      const int32_t* b = col_idx_h + row_ptr_h[r];
-      const int32_t* e = col_idx_h + row_ptr_h[r + 1];
-      const int32_t* it = std::lower_bound(b, e, c);
-      return (it != e && *it == c) ? (int32_t)(it - col_idx_h) : -1;
-    };
-    const std::string fptx = psp::gen_factor_ptx(gi), sptx = psp::gen_solve_ptx(gi);
-    h->gen_ok = psp::build_gen_kernels(fptx, sptx, (int)h->opt_codegen, !host_only, h->gen, h->gen_msg);
-    if (host_only) h->gen_ok = false;
-  } else if (h->opt_codegen > 0) {
-    h->gen_msg = "pattern above the code-generation limit (factor fma per lane > limit)";
-  }
+    CUDA_TRY(h, psp::configure_kernels(P, h->launch, (int)h->opt_groups, (int)h->opt_warps));
   h->plan = P;
   h->perm = perm;
   h->n = n;
@@ -449,7 +406,10 @@ psp_status psp_get_symbolic_info(psp_handle h, psp_symbolic_info* info, int32_t*
   info->factor_div = h->nnz_L;
   info->solve_fma = h->solve_fma;
   info->max_live = h->max_live;
-  info->kernel_variant = h->gen_ok ? 0 : h->launch.f_pend_smem ? (h->launch.f_a_smem ? 1 : 2) : 3;
+  info->factor_groups = h->launch.f_groups;
+  info->factor_warps_per_cta = h->launch.f_warps;
+  info->factor_pend_smem = h->launch.f_pend_smem ? 1 : 0;
+  info->solve_live_smem = h->launch.s_live_smem ? 1 : 0;
   info->solve_live = h->y_slots + h->x_slots;
   info->births = h->f_births;
   if (perm_h) std::copy(h->perm.begin(), h->perm.end(), perm_h);
@@ -462,7 +422,7 @@ psp_status psp_set_perturbations(psp_handle h, int32_t K, const double* eps_h, c
   if (!h->analysed) return fail(h, PSP_ERR_STATE, "psp_symbolic_analyse first");
   if (K < 1 || !eps_h || !d_h) return fail(h, PSP_ERR_ARG, "K >= 1, eps_h and d_h required");
   cudaSetDevice(h->device);
-  const int32_t Kp = (K + kSlab - 1) / kSlab * kSlab;
+  const int32_t Kp = (K + kBlock - 1) / kBlock * kBlock;
   std::vector<double> eps(Kp);
   for (int32_t k = 0; k < Kp; ++k) eps[k] = eps_h[k < K ? k : K - 1];  // pad: repeat last lane
   std::vector<double> dperm(h->n);
@@ -475,7 +435,6 @@ psp_status psp_set_perturbations(psp_handle h, int32_t K, const double* eps_h, c
   if ((s = ensure(h, h->V_d, sizeof(double) * (size_t)Kp * h->nnz_LU))) return s;
   if ((s = ensure(h, h->tol_d, sizeof(double)))) return s;
   if ((s = ensure(h, h->flag_d, sizeof(int32_t)))) return s;
-  if ((s = ensure(h, h->flags_d, sizeof(int32_t) * (Kp / psp::kSlab)))) return s;
   CUDA_TRY(h, cudaMemcpy(h->eps_d.p, eps.data(), sizeof(double) * Kp, cudaMemcpyHostToDevice));
   CUDA_TRY(h, cudaMemcpy(h->dperm_d.p, dperm.data(), sizeof(double) * h->n, cudaMemcpyHostToDevice));
   CUDA_TRY(h, cudaMemset(h->flag_d.p, 0, sizeof(int32_t)));
@@ -499,34 +458,16 @@ psp_status psp_factor_batch(psp_handle h, const double* A_vals, double pivot_tol
   }
   if (!h->launch.f_pend_smem) {
     psp_status s;
-    size_t need = sizeof(double) * (size_t)h->K_pad * (h->plan.f_slots + 2 * h->plan.c_max);
+    size_t need = sizeof(double) * (size_t)h->K_pad * h->plan.f_slots;
     if (h->fscratch_d.bytes < need) {
       CUDA_TRY(h, cudaStreamSynchronize(h->stream));
       if ((s = ensure(h, h->fscratch_d, need))) return s;
     }
   }
-  const int32_t* only = nullptr;
-  if (h->gen_ok) {
-    // generated kernel, then the interpreter re-runs only the slabs it flagged
-    CUDA_TRY(h, cudaMemsetAsync(h->flags_d.p, 0, sizeof(int32_t) * (h->K_pad / psp::kSlab), h->stream));
-    const double* A_ = A_vals;
-    const double* e_ = (const double*)h->eps_d.p;
-    const double* d_ = (const double*)h->dperm_d.p;
-    const double* t_ = tol_dev;
-    double* V_ = (double*)h->V_d.p;
-    int32_t* s_ = (int32_t*)h->status_d.p;
-    int32_t* f_ = (int32_t*)h->flags_d.p;
-    double tv = pivot_tol;
-    int32_t kp = h->K_pad;
-    void* args[] = {&A_, &e_, &d_, &t_, &V_, &s_, &f_, &tv, &kp};
-    CUDA_TRY(h, cudaLaunchKernel((const void*)h->gen.factor, dim3((h->K_pad + 127) / 128), dim3(128),
-                                 args, 0, h->stream));
-    only = f_;
-  }
   CUDA_TRY(h, psp::launch_factor(h->plan, h->launch, A_vals, (const double*)h->eps_d.p,
                                  (const double*)h->dperm_d.p, tol_dev, pivot_tol,
                                  (double*)h->V_d.p, (double*)h->fscratch_d.p,
-                                 (int32_t*)h->status_d.p, h->K_pad, only, h->stream));
+                                 (int32_t*)h->status_d.p, h->K_pad, h->stream));
   if (lane_status)
     CUDA_TRY(h, cudaMemcpyAsync(lane_status, h->status_d.p, sizeof(int32_t) * h->K,
                                 cudaMemcpyDeviceToDevice, h->stream));
@@ -553,22 +494,8 @@ psp_status psp_solve_batch(psp_handle h, int32_t R, const double* B, int64_t ldb
       if ((s = ensure(h, h->sscratch_d, need2))) return s;
     }
   }
-  const int32_t* only = nullptr;
-  if (h->gen_ok) {
-    CUDA_TRY(h, cudaMemsetAsync(h->flags_d.p, 0, sizeof(int32_t) * (h->K_pad / psp::kSlab), h->stream));
-    const double* V_ = (const double*)h->V_d.p;
-    const double* B_ = B;
-    double* X_ = (double*)h->X_d.p;
-    int32_t* f_ = (int32_t*)h->flags_d.p;
-    uint64_t ld = (uint64_t)ldb;
-    int32_t R_ = R, kp = h->K_pad;
-    void* args[] = {&V_, &B_, &X_, &f_, &ld, &R_, &kp};
-    CUDA_TRY(h, cudaLaunchKernel((const void*)h->gen.solve, dim3((h->K_pad + 127) / 128), dim3(128),
-                                 args, 0, h->stream));
-    only = f_;
-  }
   CUDA_TRY(h, psp::launch_solve(h->plan, h->launch, (const double*)h->V_d.p, B, ldb, R,
-                                (double*)h->X_d.p, (double*)h->sscratch_d.p, h->K_pad, only,
+                                (double*)h->X_d.p, (double*)h->sscratch_d.p, h->K_pad,
                                 h->stream));
   h->R = R;
   h->solved = true;
@@ -580,6 +507,18 @@ psp_status psp_get_solutions(psp_handle h, double* X) {
   if (!h->solved) return fail(h, PSP_ERR_STATE, "solve_batch first");
   CUDA_TRY(h, psp::launch_gather_solutions(h->plan, h->K, h->R, (const double*)h->X_d.p, X,
                                            h->stream));
+  return PSP_OK;
+}
+
+psp_status psp_get_factor(psp_handle h, int32_t k, double* vals_h) {
+  if (!h || !vals_h) return PSP_ERR_ARG;
+  if (!h->factored) return fail(h, PSP_ERR_STATE, "factor_batch first");
+  if (k < 0 || k >= h->K) return fail(h, PSP_ERR_ARG, "lane %d out of range", k);
+  const int L = kBlock / h->launch.f_groups;
+  const double* src = (const double*)h->V_d.p + (size_t)(k / L) * h->nnz_LU * L + (k % L);
+  CUDA_TRY(h, cudaMemcpy2DAsync(vals_h, sizeof(double), src, sizeof(double) * L, sizeof(double),
+                                (size_t)h->nnz_LU, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   return PSP_OK;
 }
 

@@ -7,62 +7,71 @@
 
 namespace psp {
 
-// Lanes are grouped in slabs of kSlab consecutive lanes (one warp, one thread per
-// lane).  Every batch-major array is laid out [slab][item][kSlab]: a warp's 32 lanes
-// of one item are 256 contiguous bytes (one coalesced access), and a slab's whole
-// factor is one contiguous region.
-constexpr int kSlab = 32;
-constexpr int kRowBytes = kSlab * 8;   // one item of one slab
+// Lanes (perturbed systems) are padded to a multiple of kBlock = 32.  The factor
+// kernel works on slabs of L = 32 / G lanes: one warp = G thread groups of L
+// threads, all groups working on the SAME L lanes (each group takes a different
+// subset of the independent updates of a pivot).  Batch-major arrays
+// are laid out [slab][item][L]; the solve kernel's warp covers kBlock = 32 lanes =
+// G consecutive factor slabs; X is [lane / 32][R][n][32].
+constexpr int kBlock = 32;
 // Source codes of the factor program: >= 0 pending slot; kZero = structural zero;
 // otherwise A[-1 - code].
 constexpr int32_t kZero = INT32_MIN;
-constexpr int kStages = 3;             // depth of every shared-memory streaming ring
-constexpr int kDataRows = 16;          // factor rows per stage of the solve's data ring
+constexpr int kStages = 4;            // depth of the CTA-shared program ring
+constexpr int kDataStages = 3;        // depth of the solve's per-warp factor-row ring
+constexpr int kDataRows = 16;         // factor rows per stage of that ring
+constexpr int kMaxWarpsCta = 16;      // consumer warps per CTA (plus one producer warp)
+
+// Record types of the programs (bits 28..31 of a record's first word).
+enum : uint32_t { kRecBirth = 1u, kRecPivot = 2u, kRecUpdate = 3u, kRecEnd = 4u, kRecYEnd = 5u };
 
 // Device-side programs (see psp_plan.cpp for their meaning).
 struct DevicePlan {
   int32_t n = 0, nnz_A = 0, nnz_LU = 0, nnz_L = 0, c_max = 0;
   const int32_t* perm = nullptr;       // [n]  perm[new] = old
-  // factor program (record stream in chunks)
+  const int32_t* adiag = nullptr;      // [n]  CSR index of A(perm[i], perm[i]) or -1
+  // factor program (records packed in chunks of f_chunk_words)
   int32_t f_slots = 0, f_chunk_words = 0, f_nchunks = 0;
   const int32_t* f_stream = nullptr;
-  // forward (ascending) and backward (descending) substitution programs
-  int32_t y_slots = 0, y_chunk_words = 0, y_nchunks = 0;
-  int32_t x_slots = 0, x_chunk_words = 0, x_nchunks = 0;
-  const int32_t* y_stream = nullptr;
-  const int32_t* x_stream = nullptr;
+  // solve program: forward (ascending) records, YEND, backward (descending) records, END
+  int32_t y_slots = 0, x_slots = 0, s_chunk_words = 0, s_nchunks = 0;
+  const int32_t* s_stream = nullptr;
   // deterministic column sums for the default pivot tolerance
   const int32_t* acsc_ptr = nullptr;   // [n+1]
   const int32_t* acsc_q = nullptr;     // [nnz_A]
 };
 
-// Launch configuration chosen per plan (host, psp_kernels.cu: configure_kernels).
+// Launch configuration chosen per plan (host, psp_kernels.cu: choose_launch).
 struct LaunchInfo {
   // factor
+  int f_groups = 1;            // G: thread groups per warp (L = 32 / G lanes per slab)
   bool f_pend_smem = false;    // pending slots in shared memory (else global scratch)
-  bool f_a_smem = false;       // A values and d staged in shared memory
-  int f_warps = 1;             // warps (slabs) per CTA
+  int f_warps = 1;             // consumer warps (slabs) per CTA
   int f_smem = 0;              // dynamic shared memory per CTA
-  int f_off_a = 0, f_off_d = 0, f_off_warp = 0, f_warp_bytes = 0;
+  int f_off_warp = 0, f_warp_bytes = 0, f_off_scr = 0;
+  int f_ctas_per_sm = 0;
   // solve
   bool s_live_smem = false;
   int s_warps = 1;
   int s_smem = 0;
-  int s_off_b = 0, s_off_warp = 0, s_warp_bytes = 0, s_ring_bytes = 0;
+  int s_off_b = 0, s_off_warp = 0, s_warp_bytes = 0, s_off_data = 0;
+  int s_ctas_per_sm = 0;
 };
 
 // Kernel launchers (psp_kernels.cu).  All asynchronous on `stream`.
-void choose_launch(const DevicePlan& p, LaunchInfo& li);   // pure host logic
-cudaError_t configure_kernels(const DevicePlan& p, LaunchInfo& li);
+// force_groups: 0 = automatic, else G in {1, 2, 4, 8}; force_warps: 0 = automatic.
+void choose_launch(const DevicePlan& p, LaunchInfo& li, int force_groups, int force_warps);
+cudaError_t configure_kernels(const DevicePlan& p, LaunchInfo& li, int force_groups,
+                              int force_warps);
 cudaError_t launch_pivot_tol(const DevicePlan& p, const double* A_vals, double* tol_out,
                              cudaStream_t stream);
 cudaError_t launch_factor(const DevicePlan& p, const LaunchInfo& li, const double* A_vals,
                           const double* eps, const double* dperm, const double* tol_dev,
                           double tol_value, double* V, double* gscratch, int32_t* status,
-                          int32_t K_pad, const int32_t* only, cudaStream_t stream);
+                          int32_t K_pad, cudaStream_t stream);
 cudaError_t launch_solve(const DevicePlan& p, const LaunchInfo& li, const double* V,
                          const double* B, int64_t ldb, int32_t R, double* X, double* gscratch,
-                         int32_t K_pad, const int32_t* only, cudaStream_t stream);
+                         int32_t K_pad, cudaStream_t stream);
 cudaError_t launch_recover(const DevicePlan& p, int32_t W, int32_t R, const int32_t* w_ptr,
                            const int32_t* w_lane, const double* w_val, const double* X,
                            const int32_t* status, double* x_out, int32_t* infeasible_flag,

@@ -21,6 +21,7 @@
 // first update and dies when its pivot consumes it.  Slots are reused greedily
 // (interval colouring), so the slot count equals the peak pending set.
 #include "psp_plan.h"
+#include "psp_internal.h"
 
 #include <algorithm>
 #include <climits>
@@ -168,11 +169,12 @@ int32_t colour(int32_t n_steps, const std::vector<int32_t>& birth, const std::ve
 }
 
 // Pack 16-byte-aligned records into fixed-size chunks (the kernels stream chunks
-// into shared-memory rings with bulk async copies).  A record never straddles a
-// chunk; the rest of a chunk after its last record starts with the sentinel -1.
+// into a CTA-shared shared-memory ring with bulk async copies).  A record never
+// straddles a chunk; the rest of a chunk after its last record starts with the
+// sentinel -1 (there are always >= 4 words of it).
 void pack_chunks(const std::vector<std::vector<int32_t>>& recs, size_t max_rec,
                  int32_t& chunk_words, std::vector<int32_t>& out) {
-  chunk_words = 256;  // 1 KB
+  chunk_words = 512;  // 2 KB
   while ((size_t)chunk_words < max_rec + 4) chunk_words *= 2;
   out.assign(chunk_words, -1);
   size_t base = 0, used = 0;
@@ -271,40 +273,46 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
     return q >= 0 ? -1 - q : INT_MIN;
   };
   // Factor stream (records 16-byte aligned, packed into fixed-size chunks that the
-  // kernel pulls into a shared-memory ring with bulk async copies):
-  //   BIRTH  [1<<28 | nb, 0, 0, 0] + nb x (slot, A index or -1, d index or -1), nb <= 64
-  //   PIVOT  [2<<28 | c, pivot source, lofs, dofs] + c L sources + c U sources
-  //   UPDATE [3<<28 | j0, a0, na, w] + na int4 rows of 8 uint16 target slots:
-  //          rows a0..a0+na-1, columns j0..j0+w-1 of the pivot's c x c block
-  //   UPDATE32 [5<<28 | j0, a0, na, w] + na x 8 int32 slots (pending sets >= 65536)
+  // kernel pulls into a CTA-shared ring with bulk async copies):
+  //   BIRTH  [1<<28 | nb, 0, 0, 0] + nb x (slot | diag << 31, diag ? i : A index or -1),
+  //          nb <= 64: pending slot <- A value (+ eps*d_i on the diagonal, or 0 for fill)
+  //   PIVOT  [2<<28 | c, pivot source, p, 0] + c L sources + c U sources
+  //   UPDATE [3<<28 | w, a0, na, j0] + na x 8 int32 target slots: rows a0..a0+na-1,
+  //          columns j0..j0+w-1 of the pivot's c x c block (unused columns 0)
   //   END    [4<<28, 0, 0, 0]
+  // The output position of pivot p (lofs[p], dofs[p]) is implicit: pivots come in order.
   std::vector<std::vector<int32_t>> recs;
   size_t max_rec = 0;
   P.f_births = 0;
-  const bool wide = P.f_slots + 2 * P.c_max > 65535;
   auto push = [&](std::vector<int32_t>&& r) {
     while (r.size() % 4) r.push_back(0);
     max_rec = std::max(max_rec, r.size());
     recs.push_back(std::move(r));
   };
+  P.adiag.assign(n, -1);
+  for (int32_t i = 0; i < n; ++i) P.adiag[i] = a_index(i, i);
   for (int32_t p = 0; p < n; ++p) {
     const auto& L = lcol[p];
     const int32_t c = (int32_t)L.size();
     const auto& bl = births_at[p];
     for (size_t b0 = 0; b0 < bl.size(); b0 += 64) {
       const size_t b1 = std::min(bl.size(), b0 + 64);
-      std::vector<int32_t> r = {(int32_t)((1u << 28) | (uint32_t)(b1 - b0)), 0, 0, 0};
+      std::vector<int32_t> r = {(int32_t)((kRecBirth << 28) | (uint32_t)(b1 - b0)), 0, 0, 0};
       for (size_t q = b0; q < b1; ++q) {
         const int32_t e = bl[q], i = ent_i[e], j = ent_j[e];
-        r.push_back(fslot[e]);
-        r.push_back(a_index(i, j));
-        r.push_back(i == j ? i : -1);
+        if (i == j) {
+          r.push_back((int32_t)((uint32_t)fslot[e] | 0x80000000u));
+          r.push_back(i);
+        } else {
+          r.push_back(fslot[e]);
+          r.push_back(a_index(i, j));
+        }
         ++P.f_births;
       }
       push(std::move(r));
     }
     {
-      std::vector<int32_t> r = {(int32_t)((2u << 28) | (uint32_t)c), src_code(p, p), P.lofs[p], P.dofs[p]};
+      std::vector<int32_t> r = {(int32_t)((kRecPivot << 28) | (uint32_t)c), src_code(p, p), p, 0};
       for (int32_t k = 0; k < c; ++k) r.push_back(src_code(L[k], p));
       for (int32_t k = 0; k < c; ++k) r.push_back(src_code(p, L[k]));
       push(std::move(r));
@@ -313,27 +321,34 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
       const int32_t wdt = std::min(8, c - j0);
       for (int32_t a0 = 0; a0 < c; a0 += 32) {
         const int32_t na = std::min(32, c - a0);
-        std::vector<int32_t> r = {(int32_t)(((wide ? 5u : 3u) << 28) | (uint32_t)j0), a0, na, wdt};
-        for (int32_t a = a0; a < a0 + na; ++a) {
-          if (wide) {  // 8 int32 slots per row (two int4)
-            for (int32_t b = 0; b < 8; ++b)
-              r.push_back(b < wdt ? fslot[entry(L[a], L[j0 + b])] : 0);
-            continue;
-          }
-          for (int32_t b = 0; b < 8; b += 2) {
-            const int32_t c0 = j0 + b, c1 = c0 + 1;
-            const uint32_t s0 = b < wdt ? (uint32_t)fslot[entry(L[a], L[c0])] : 0u;
-            const uint32_t s1 = b + 1 < wdt ? (uint32_t)fslot[entry(L[a], L[c1])] : 0u;
-            r.push_back((int32_t)(s0 | (s1 << 16)));
-          }
-        }
+        std::vector<int32_t> r = {(int32_t)((kRecUpdate << 28) | (uint32_t)wdt), a0, na, j0};
+        for (int32_t a = a0; a < a0 + na; ++a)
+          for (int32_t b = 0; b < 8; ++b) r.push_back(b < wdt ? fslot[entry(L[a], L[j0 + b])] : 0);
         push(std::move(r));
       }
     }
   }
-  push({(int32_t)(4u << 28), 0, 0, 0});
+  push({(int32_t)(kRecEnd << 28), 0, 0, 0});
   pack_chunks(recs, max_rec, P.f_chunk_words, P.f_stream);
-  // ---------------- forward substitution (column-oriented, ascending) ----------
+
+  // ---------------- solve program ----------------
+  // Forward substitution (column-oriented, pivots ascending):
+  //   YBIRTH [1<<28 | nb, 0, 0, 0] + nb x (slot, original row): pending y_i <- b[row]
+  //   YPIVOT [2<<28 | c, ys, lofs, 0] + c target slots: y_j final (slot ys, or b if
+  //          never updated); y_i = fma(-l_ij, y_j, y_i) for the c rows of L(:, j)
+  //   YEND   [5<<28, 0, 0, 0]
+  // Backward substitution (row-oriented, pivots descending, the sum in descending
+  // column order, the division last):
+  //   XROW   [3<<28 | c, xs, dofs, i] + c slots of x_{i_k}; xs = slot keeping x_i for
+  //          the rows above that need it (or -1)
+  //   END    [4<<28, 0, 0, 0]
+  std::vector<std::vector<int32_t>> srec;
+  size_t smax = 0;
+  auto spush = [&](std::vector<int32_t>&& r) {
+    while (r.size() % 4) r.push_back(0);
+    smax = std::max(smax, r.size());
+    srec.push_back(std::move(r));
+  };
   {
     std::vector<int32_t> yb(n, -1), yd(n, -1);
     for (int32_t j = 0; j < n; ++j)
@@ -347,37 +362,27 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
     std::vector<std::vector<int32_t>> yborn(n);
     for (int32_t i = 0; i < n; ++i)
       if (yb[i] >= 0) yborn[yb[i]].push_back(i);
-    std::vector<std::vector<int32_t>> yrec;
-    size_t ymax = 0;
-    auto ypush = [&](std::vector<int32_t>&& r) {
-      while (r.size() % 4) r.push_back(0);
-      ymax = std::max(ymax, r.size());
-      yrec.push_back(std::move(r));
-    };
-    // YBIRTH [1<<28 | nb, 0, 0, 0] + nb x (slot, original row);  YPIVOT [2<<28 | c, ys, lofs, 0]
-    // + c target slots;  END [4<<28, ...]
     for (int32_t j = 0; j < n; ++j) {
       const auto& bl = yborn[j];
       for (size_t b0 = 0; b0 < bl.size(); b0 += 64) {
         const size_t b1 = std::min(bl.size(), b0 + 64);
-        std::vector<int32_t> r = {(int32_t)((1u << 28) | (uint32_t)(b1 - b0)), 0, 0, 0};
+        std::vector<int32_t> r = {(int32_t)((kRecBirth << 28) | (uint32_t)(b1 - b0)), 0, 0, 0};
         for (size_t q = b0; q < b1; ++q) {
           r.push_back(ys[bl[q]]);
           r.push_back(perm[bl[q]]);
         }
-        ypush(std::move(r));
+        spush(std::move(r));
       }
-      std::vector<int32_t> r = {(int32_t)((2u << 28) | (uint32_t)lcol[j].size()),
+      std::vector<int32_t> r = {(int32_t)((kRecPivot << 28) | (uint32_t)lcol[j].size()),
                                 yb[j] >= 0 ? ys[j] : -1, P.lofs[j], 0};
       for (int32_t i : lcol[j]) r.push_back(ys[i]);
-      ypush(std::move(r));
+      spush(std::move(r));
     }
-    ypush({(int32_t)(4u << 28), 0, 0, 0});
-    pack_chunks(yrec, ymax, P.y_chunk_words, P.y_stream);
+    spush({(int32_t)(kRecYEnd << 28), 0, 0, 0});
   }
-  // ---------------- backward substitution (row-oriented, descending) ----------
   {
-    // step s = n-1-i; x_i born at step of i, dies at the step of the smallest q with i in lcol(q)
+    // step s = n-1-i; x_i born at the step of i, dies at the step of the smallest q with
+    // i in lcol(q)
     std::vector<int32_t> xb(n, -1), xd(n, -1);
     for (int32_t q = 0; q < n; ++q)
       for (int32_t i : lcol[q])
@@ -386,18 +391,15 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
       if (xd[i] >= 0) xb[i] = n - 1 - i;
     std::vector<int32_t> xs;
     P.x_slots = colour(n, xb, xd, true, xs);
-    // records in processing order (pivots descending)
-    std::vector<std::vector<int32_t>> xrec;
-    size_t xmax = 0;
     for (int32_t i = n - 1; i >= 0; --i) {
-      std::vector<int32_t> xc = {(int32_t)lcol[i].size(), xb[i] >= 0 ? xs[i] : -1, P.dofs[i], i};
-      for (int32_t k : lcol[i]) xc.push_back(xs[k]);
-      while (xc.size() % 4) xc.push_back(0);
-      xmax = std::max(xmax, xc.size());
-      xrec.push_back(std::move(xc));
+      std::vector<int32_t> r = {(int32_t)((kRecUpdate << 28) | (uint32_t)lcol[i].size()),
+                                xb[i] >= 0 ? xs[i] : -1, P.dofs[i], i};
+      for (int32_t k : lcol[i]) r.push_back(xs[k]);
+      spush(std::move(r));
     }
-    pack_chunks(xrec, xmax, P.x_chunk_words, P.x_stream);
+    spush({(int32_t)(kRecEnd << 28), 0, 0, 0});
   }
+  pack_chunks(srec, smax, P.s_chunk_words, P.s_stream);
 }
 
 }  // namespace psp

@@ -19,11 +19,13 @@ struct HostPlan {
   // per-lane factor layout: L region (column p of L at lofs[p], c_p values) followed
   // by the DU region (u_pp then U row p at nnz_L + dofs[p], 1 + c_p values)
   std::vector<int32_t> lofs, dofs;  // [n+1]
-  // factor / forward / backward programs: record streams packed in chunks
+  std::vector<int32_t> adiag;       // [n] CSR index of A's diagonal (permuted numbering) or -1
+  // factor program and solve program (forward records, YEND, backward records, END):
+  // record streams packed in chunks
   int32_t f_slots = 0, f_births = 0, f_chunk_words = 0;
   std::vector<int32_t> f_stream;
-  int32_t y_slots = 0, x_slots = 0, y_chunk_words = 0, x_chunk_words = 0;
-  std::vector<int32_t> y_stream, x_stream;
+  int32_t y_slots = 0, x_slots = 0, s_chunk_words = 0;
+  std::vector<int32_t> s_stream;
 };
 
 std::vector<int32_t> min_degree_order(int32_t n, const std::vector<std::vector<int32_t>>& adj,

@@ -10,7 +10,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpsp.so")
+LIB_PATH = os.environ.get("PSP_LIB", os.path.join(_HERE, "libpsp.so"))
 
 PSP_OK = 0
 STATUS = {0: "PSP_OK", 1: "PSP_ERR_ARG", 2: "PSP_ERR_DIM", 3: "PSP_ERR_STATE",
@@ -24,8 +24,8 @@ EXPORTS = ["psp_create", "psp_destroy", "psp_set_stream", "psp_status_string",
            "psp_last_error_detail", "psp_symbolic_analyse", "psp_get_symbolic_info",
            "psp_set_perturbations", "psp_factor_batch", "psp_solve_batch", "psp_get_solutions",
            "psp_set_weights", "psp_recover", "psp_get_lane_status", "psp_solve_host",
-           "psp_synchronize", "psp_ladder_weights", "psp_set_option", "psp_codegen_status"]
-OPT = {"codegen": 1, "codegen_max_fma": 2, "max_regs": 3}
+           "psp_synchronize", "psp_ladder_weights", "psp_set_option", "psp_get_factor"]
+OPT = {"factor_groups": 1, "factor_warps": 2}
 
 
 class SymbolicInfo(ctypes.Structure):
@@ -33,8 +33,10 @@ class SymbolicInfo(ctypes.Structure):
                 ("nnz_L", ctypes.c_int32), ("n_struct_zero_diag", ctypes.c_int32),
                 ("n_levels", ctypes.c_int32), ("factor_fma", ctypes.c_int64),
                 ("factor_div", ctypes.c_int64), ("solve_fma", ctypes.c_int64),
-                ("max_live", ctypes.c_int32), ("kernel_variant", ctypes.c_int32),
-                ("solve_live", ctypes.c_int32), ("births", ctypes.c_int32)]
+                ("max_live", ctypes.c_int32), ("solve_live", ctypes.c_int32),
+                ("births", ctypes.c_int32), ("factor_groups", ctypes.c_int32),
+                ("factor_warps_per_cta", ctypes.c_int32), ("factor_pend_smem", ctypes.c_int32),
+                ("solve_live_smem", ctypes.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -74,6 +76,7 @@ def lib():
             "psp_solve_host": [P, P, I32, P, D, P],
             "psp_ladder_weights": [I32, P, P, P],
             "psp_set_option": [P, I32, I64],
+            "psp_get_factor": [P, I32, P],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -83,8 +86,6 @@ def lib():
         L.psp_status_string.restype = ctypes.c_char_p
         L.psp_last_error_detail.argtypes = [P]
         L.psp_last_error_detail.restype = ctypes.c_char_p
-        L.psp_codegen_status.argtypes = [P]
-        L.psp_codegen_status.restype = ctypes.c_char_p
         _lib = L
     return _lib
 
@@ -131,18 +132,15 @@ class Solver:
         return st
 
     def close(self):
-        if getattr(self, "h", None) is not None and self.h:
-            lib().psp_destroy(self.h)
-            self.h = None
+        if getattr(self, "h", None) is not None and self.h and _lib is not None:
+            _lib.psp_destroy(self.h)
+        self.h = None
 
     __del__ = close
 
     # --- C-ABI wrappers ------------------------------------------------------
     def psp_set_option(self, name, value):
         self._check(lib().psp_set_option(self.h, OPT[name], int(value)))
-
-    def psp_codegen_status(self):
-        return lib().psp_codegen_status(self.h).decode()
 
     def psp_symbolic_analyse(self, n, row_ptr, col_idx, ordering="mindeg", user_perm=None, first_node=-1):
         rp = np.ascontiguousarray(row_ptr, dtype=np.int32)
@@ -187,6 +185,12 @@ class Solver:
         out = out if out is not None else self.torch.empty((self.K, self.R, self.n), dtype=self.torch.float64,
                                                            device=f"cuda:{self.device}")
         self._check(lib().psp_get_solutions(self.h, _t_ptr(out)))
+        return out
+
+    def psp_get_factor(self, k, nnz_LU):
+        """Lane k's factor values (host numpy, pivot-major layout of include/psp.h)."""
+        out = np.empty(nnz_LU, dtype=np.float64)
+        self._check(lib().psp_get_factor(self.h, int(k), _np_ptr(out)))
         return out
 
     def psp_set_weights(self, w_ptr, w_lane, w_val):
@@ -261,9 +265,6 @@ class HostSymbolic:
         if st:
             raise PSPError(st, lib().psp_last_error_detail(self.h).decode())
 
-    def codegen_status(self):
-        return lib().psp_codegen_status(self.h).decode()
-
     def analyse(self, n, row_ptr, col_idx, ordering="mindeg", user_perm=None, first_node=-1):
         rp = np.ascontiguousarray(row_ptr, dtype=np.int32)
         ci = np.ascontiguousarray(col_idx, dtype=np.int32)
@@ -280,8 +281,8 @@ class HostSymbolic:
         return info.as_dict(), perm
 
     def close(self):
-        if self.h:
-            lib().psp_destroy(self.h)
-            self.h = None
+        if self.h and _lib is not None:
+            _lib.psp_destroy(self.h)
+        self.h = None
 
     __del__ = close
