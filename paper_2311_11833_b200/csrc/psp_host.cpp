@@ -356,6 +356,8 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
   P.f_slots = HP.f_slots;
   P.f_chunk_words = HP.f_chunk_words;
   P.f_nchunks = (int32_t)(HP.f_stream.size() / HP.f_chunk_words);
+  P.c_scr = HP.c_max > psp::kFusedMax ? HP.c_max : 0;
+  P.f_npatch = (int32_t)HP.f_patch_pos.size();
   P.y_slots = HP.y_slots;
   P.x_slots = HP.x_slots;
   P.s_chunk_words = HP.s_chunk_words;
@@ -365,14 +367,18 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
   if (!host_only && (s = upload(h, vec, &P.field))) return s;
   UP(perm, perm);
   UP(HP.adiag, adiag);
-  UP(HP.f_stream, f_stream);
+  UP(HP.f_stream, f_stream);   // patched in place with A and d before every factorisation
+  UP(HP.f_patch_pos, f_patch_pos);
+  UP(HP.f_patch_src, f_patch_src);
   UP(HP.s_stream, s_stream);
   UP(acsc_ptr, acsc_ptr);
   UP(acsc_q, acsc_q);
 #undef UP
-  if (host_only)
-    psp::choose_launch(P, h->launch, (int)h->opt_groups, (int)h->opt_warps);
-  else
+  if (!psp::choose_launch(P, h->launch, (int)h->opt_groups, (int)h->opt_warps))
+    return fail(h, PSP_ERR_UNSUPPORTED, "no kernel configuration fits shared memory "
+                "(program chunk %d words, c_max %d, solve live slots %d)", P.f_chunk_words,
+                P.c_max, P.y_slots + P.x_slots);
+  if (!host_only)
     CUDA_TRY(h, psp::configure_kernels(P, h->launch, (int)h->opt_groups, (int)h->opt_warps));
   h->plan = P;
   h->perm = perm;
@@ -464,9 +470,10 @@ psp_status psp_factor_batch(psp_handle h, const double* A_vals, double pivot_tol
       if ((s = ensure(h, h->fscratch_d, need))) return s;
     }
   }
-  CUDA_TRY(h, psp::launch_factor(h->plan, h->launch, A_vals, (const double*)h->eps_d.p,
-                                 (const double*)h->dperm_d.p, tol_dev, pivot_tol,
-                                 (double*)h->V_d.p, (double*)h->fscratch_d.p,
+  CUDA_TRY(h, psp::launch_patch_program(h->plan, const_cast<int32_t*>(h->plan.f_stream), A_vals,
+                                        (const double*)h->dperm_d.p, h->stream));
+  CUDA_TRY(h, psp::launch_factor(h->plan, h->launch, h->plan.f_stream, (const double*)h->eps_d.p,
+                                 tol_dev, pivot_tol, (double*)h->V_d.p, (double*)h->fscratch_d.p,
                                  (int32_t*)h->status_d.p, h->K_pad, h->stream));
   if (lane_status)
     CUDA_TRY(h, cudaMemcpyAsync(lane_status, h->status_d.p, sizeof(int32_t) * h->K,

@@ -14,13 +14,13 @@ namespace psp {
 // are laid out [slab][item][L]; the solve kernel's warp covers kBlock = 32 lanes =
 // G consecutive factor slabs; X is [lane / 32][R][n][32].
 constexpr int kBlock = 32;
-// Source codes of the factor program: >= 0 pending slot; kZero = structural zero;
-// otherwise A[-1 - code].
-constexpr int32_t kZero = INT32_MIN;
+// Source codes of the factor program: >= 0 pending slot; otherwise A[-1 - code] of A
+// extended by one structural zero, A[nnz_A] = 0.
 constexpr int kStages = 4;            // depth of the CTA-shared program ring
 constexpr int kDataStages = 3;        // depth of the solve's per-warp factor-row ring
 constexpr int kDataRows = 16;         // factor rows per stage of that ring
 constexpr int kMaxWarpsCta = 16;      // consumer warps per CTA (plus one producer warp)
+constexpr int kFusedMax = 16;         // pivots with c <= kFusedMax: u in registers, no scratch
 
 // Record types of the programs (bits 28..31 of a record's first word).
 enum : uint32_t { kRecBirth = 1u, kRecPivot = 2u, kRecUpdate = 3u, kRecEnd = 4u, kRecYEnd = 5u };
@@ -31,8 +31,11 @@ struct DevicePlan {
   const int32_t* perm = nullptr;       // [n]  perm[new] = old
   const int32_t* adiag = nullptr;      // [n]  CSR index of A(perm[i], perm[i]) or -1
   // factor program (records packed in chunks of f_chunk_words)
-  int32_t f_slots = 0, f_chunk_words = 0, f_nchunks = 0;
-  const int32_t* f_stream = nullptr;
+  int32_t f_slots = 0, f_chunk_words = 0, f_nchunks = 0, c_scr = 0;  // c_scr: scratch rows
+  const int32_t* f_stream = nullptr;   // the handle's patched copy (immediates filled in)
+  int32_t f_npatch = 0;
+  const int32_t* f_patch_pos = nullptr;
+  const int32_t* f_patch_src = nullptr;
   // solve program: forward (ascending) records, YEND, backward (descending) records, END
   int32_t y_slots = 0, x_slots = 0, s_chunk_words = 0, s_nchunks = 0;
   const int32_t* s_stream = nullptr;
@@ -60,15 +63,19 @@ struct LaunchInfo {
 
 // Kernel launchers (psp_kernels.cu).  All asynchronous on `stream`.
 // force_groups: 0 = automatic, else G in {1, 2, 4, 8}; force_warps: 0 = automatic.
-void choose_launch(const DevicePlan& p, LaunchInfo& li, int force_groups, int force_warps);
+// Returns false when no configuration fits the shared memory (the program's records or
+// the solve's working set are too large).
+bool choose_launch(const DevicePlan& p, LaunchInfo& li, int force_groups, int force_warps);
 cudaError_t configure_kernels(const DevicePlan& p, LaunchInfo& li, int force_groups,
                               int force_warps);
+// Fill the factor stream's immediates (A values, d) in `stream_out` (device copy).
+cudaError_t launch_patch_program(const DevicePlan& p, int32_t* stream_out, const double* A_vals,
+                                 const double* dperm, cudaStream_t stream);
 cudaError_t launch_pivot_tol(const DevicePlan& p, const double* A_vals, double* tol_out,
                              cudaStream_t stream);
-cudaError_t launch_factor(const DevicePlan& p, const LaunchInfo& li, const double* A_vals,
-                          const double* eps, const double* dperm, const double* tol_dev,
-                          double tol_value, double* V, double* gscratch, int32_t* status,
-                          int32_t K_pad, cudaStream_t stream);
+cudaError_t launch_factor(const DevicePlan& p, const LaunchInfo& li, const int32_t* prog,
+                          const double* eps, const double* tol_dev, double tol_value, double* V,
+                          double* gscratch, int32_t* status, int32_t K_pad, cudaStream_t stream);
 cudaError_t launch_solve(const DevicePlan& p, const LaunchInfo& li, const double* V,
                          const double* B, int64_t ldb, int32_t R, double* X, double* gscratch,
                          int32_t K_pad, cudaStream_t stream);

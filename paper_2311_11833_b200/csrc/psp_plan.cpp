@@ -173,18 +173,27 @@ int32_t colour(int32_t n_steps, const std::vector<int32_t>& birth, const std::ve
 // straddles a chunk; the rest of a chunk after its last record starts with the
 // sentinel -1 (there are always >= 4 words of it).
 void pack_chunks(const std::vector<std::vector<int32_t>>& recs, size_t max_rec,
-                 int32_t& chunk_words, std::vector<int32_t>& out) {
+                 int32_t& chunk_words, std::vector<int32_t>& out,
+                 const std::vector<std::vector<std::pair<int32_t, int32_t>>>* patches = nullptr,
+                 std::vector<int32_t>* patch_pos = nullptr,
+                 std::vector<int32_t>* patch_src = nullptr) {
   chunk_words = 512;  // 2 KB
   while ((size_t)chunk_words < max_rec + 4) chunk_words *= 2;
   out.assign(chunk_words, -1);
   size_t base = 0, used = 0;
-  for (const auto& r : recs) {
+  for (size_t k = 0; k < recs.size(); ++k) {
+    const auto& r = recs[k];
     if (used + r.size() + 4 > (size_t)chunk_words) {
       base += chunk_words;
       used = 0;
       out.resize(base + chunk_words, -1);
     }
     std::copy(r.begin(), r.end(), out.begin() + base + used);
+    if (patches)
+      for (const auto& pr : (*patches)[k]) {
+        patch_pos->push_back((int32_t)(base + used + pr.first));
+        patch_src->push_back(pr.second);
+      }
     used += r.size();
   }
 }
@@ -213,6 +222,7 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
   P.factor_fma = ffma;
   P.solve_fma = 2 * nnzL;
 
+  const int32_t nnzA = row_ptr_h[n];
   // A lookup in the permuted numbering: (i, j) -> CSR index of A(perm[i], perm[j]) or -1
   auto a_index = [&](int32_t i, int32_t j) -> int32_t {
     const int32_t r = perm[i], c = perm[j];
@@ -266,70 +276,122 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
   std::vector<std::vector<int32_t>> births_at(n);
   for (int32_t e = 0; e < n_ent; ++e)
     if (first[e] >= 0) births_at[first[e]].push_back(e);
-  auto src_code = [&](int32_t i, int32_t j) -> int32_t {
-    const int32_t e = entry(i, j);
-    if (first[e] >= 0) return fslot[e];
-    const int32_t q = a_index(i, j);
-    return q >= 0 ? -1 - q : INT_MIN;
-  };
-  // Factor stream (records 16-byte aligned, packed into fixed-size chunks that the
-  // kernel pulls into a CTA-shared ring with bulk async copies):
-  //   BIRTH  [1<<28 | nb, 0, 0, 0] + nb x (slot | diag << 31, diag ? i : A index or -1),
-  //          nb <= 64: pending slot <- A value (+ eps*d_i on the diagonal, or 0 for fill)
-  //   PIVOT  [2<<28 | c, pivot source, p, 0] + c L sources + c U sources
-  //   UPDATE [3<<28 | w, a0, na, j0] + na x 8 int32 target slots: rows a0..a0+na-1,
-  //          columns j0..j0+w-1 of the pivot's c x c block (unused columns 0)
-  //   END    [4<<28, 0, 0, 0]
-  // The output position of pivot p (lofs[p], dofs[p]) is implicit: pivots come in order.
+  // Factor stream (v4): one record per pivot, 16-byte aligned, packed into fixed-size
+  // chunks that the kernel pulls into a CTA-shared ring with bulk async copies.  Values
+  // of A and d are IMMEDIATES: 64-bit cells patched into a device copy of the stream
+  // before every factorisation (patch list f_patch_pos / f_patch_src below), so the
+  // kernel never looks A up.  An OPERAND is 4 words [slot, 0, lo, hi]: the pending slot
+  // (slot >= 0) or the immediate (lo, hi) when slot = -1.
+  //   PIVOT  [2<<28 | c, p, nbd, nba, flags, ws, d_p (2 words)]
+  //          + pivot operand (4 words)
+  //          + nbd diagonal births  [slot, 0, a_ii (2), d_i (2), 0, 0]: a_ii + eps*d_i
+  //          + nba births           [slot, 0, a_ij (2)] (structural zeros: a_ij = 0)
+  //          + c L operands, c U operands (4 words each)
+  //          + (flags & 2 == 0) c rows x ws target slots of the c x c update block
+  //          flags: 1 = the pivot was never updated (add eps*d_p); 2 = c > kFusedMax,
+  //          the update comes in UPDATE records; ws = row stride (8 * ceil(c / 8))
+  //   BIRTH  [1<<28, 0, nbd, nba, 0, 0, 0, 0] + births: those of the next pivot that do
+  //          not fit its record
+  //   UPDATE [3<<28 | c, a0, na, ws, 0, 0, 0, 0] + na rows x ws target slots (rows
+  //          a0 .. a0+na-1 of a pivot with c > kFusedMax)
+  //   END    [4<<28, ...]
+  // Births of pivot p are the entries first touched by p's update; the pivot's output
+  // position (lofs[p], dofs[p]) is implicit: pivots come in order.
+  constexpr size_t kMaxRec = 508;   // words: records stay within one 2 KB chunk
   std::vector<std::vector<int32_t>> recs;
+  std::vector<std::vector<std::pair<int32_t, int32_t>>> rec_patch;  // (word offset, src)
   size_t max_rec = 0;
   P.f_births = 0;
-  auto push = [&](std::vector<int32_t>&& r) {
+  auto pad4 = [](std::vector<int32_t>& r) {
     while (r.size() % 4) r.push_back(0);
+  };
+  auto push = [&](std::vector<int32_t>&& r, std::vector<std::pair<int32_t, int32_t>>&& pt) {
+    pad4(r);
     max_rec = std::max(max_rec, r.size());
     recs.push_back(std::move(r));
+    rec_patch.push_back(std::move(pt));
+  };
+  // immediate cell sources: >= 0 A index (nnz_A = the structural zero), < 0: d[-1 - src]
+  auto imm = [](std::vector<int32_t>& r, std::vector<std::pair<int32_t, int32_t>>& pt, int32_t src) {
+    pt.push_back({(int32_t)r.size(), src});
+    r.push_back(0);
+    r.push_back(0);
+  };
+  auto operand = [&](std::vector<int32_t>& r, std::vector<std::pair<int32_t, int32_t>>& pt,
+                     int32_t i, int32_t j) {
+    const int32_t e = entry(i, j);
+    if (first[e] >= 0) {
+      r.insert(r.end(), {fslot[e], 0, 0, 0});
+    } else {
+      const int32_t q = a_index(i, j);
+      r.insert(r.end(), {-1, 0});
+      imm(r, pt, q >= 0 ? q : nnzA);
+    }
+  };
+  auto birth = [&](std::vector<int32_t>& r, std::vector<std::pair<int32_t, int32_t>>& pt, int32_t e) {
+    const int32_t i = ent_i[e], j = ent_j[e];
+    const int32_t q = a_index(i, j);
+    r.insert(r.end(), {fslot[e], 0});
+    imm(r, pt, q >= 0 ? q : nnzA);
+    if (i == j) {
+      imm(r, pt, -1 - i);
+      r.insert(r.end(), {0, 0});
+    }
+    ++P.f_births;
   };
   P.adiag.assign(n, -1);
   for (int32_t i = 0; i < n; ++i) P.adiag[i] = a_index(i, i);
   for (int32_t p = 0; p < n; ++p) {
     const auto& L = lcol[p];
     const int32_t c = (int32_t)L.size();
-    const auto& bl = births_at[p];
-    for (size_t b0 = 0; b0 < bl.size(); b0 += 64) {
-      const size_t b1 = std::min(bl.size(), b0 + 64);
-      std::vector<int32_t> r = {(int32_t)((kRecBirth << 28) | (uint32_t)(b1 - b0)), 0, 0, 0};
-      for (size_t q = b0; q < b1; ++q) {
-        const int32_t e = bl[q], i = ent_i[e], j = ent_j[e];
-        if (i == j) {
-          r.push_back((int32_t)((uint32_t)fslot[e] | 0x80000000u));
-          r.push_back(i);
-        } else {
-          r.push_back(fslot[e]);
-          r.push_back(a_index(i, j));
-        }
-        ++P.f_births;
-      }
-      push(std::move(r));
+    const int32_t ws = 8 * ((c + 7) / 8);
+    const bool fused = c <= kFusedMax;
+    std::vector<int32_t> bd, bo;   // diagonal / other births (entry ids)
+    for (int32_t e : births_at[p]) (ent_i[e] == ent_j[e] ? bd : bo).push_back(e);
+    const size_t fixed = 8 + 4 + 8 * (size_t)c + (fused ? (size_t)c * ws : 0);
+    // births that do not fit the pivot's record go first, in BIRTH records
+    size_t qd = 0, qo = 0;
+    while (fixed + 8 * (bd.size() - qd) + 4 * (bo.size() - qo) > kMaxRec &&
+           (qd < bd.size() || qo < bo.size())) {
+      std::vector<int32_t> b = {(int32_t)(kRecBirth << 28), 0, 0, 0, 0, 0, 0, 0};
+      std::vector<std::pair<int32_t, int32_t>> pt;
+      int32_t nd = 0, no = 0;
+      while (qd < bd.size() && b.size() + 8 <= kMaxRec) birth(b, pt, bd[qd++]), ++nd;
+      while (qo < bo.size() && b.size() + 4 <= kMaxRec) birth(b, pt, bo[qo++]), ++no;
+      b[2] = nd;
+      b[3] = no;
+      push(std::move(b), std::move(pt));
     }
-    {
-      std::vector<int32_t> r = {(int32_t)((kRecPivot << 28) | (uint32_t)c), src_code(p, p), p, 0};
-      for (int32_t k = 0; k < c; ++k) r.push_back(src_code(L[k], p));
-      for (int32_t k = 0; k < c; ++k) r.push_back(src_code(p, L[k]));
-      push(std::move(r));
-    }
-    for (int32_t j0 = 0; j0 < c; j0 += 8) {
-      const int32_t wdt = std::min(8, c - j0);
-      for (int32_t a0 = 0; a0 < c; a0 += 32) {
-        const int32_t na = std::min(32, c - a0);
-        std::vector<int32_t> r = {(int32_t)((kRecUpdate << 28) | (uint32_t)wdt), a0, na, j0};
-        for (int32_t a = a0; a < a0 + na; ++a)
-          for (int32_t b = 0; b < 8; ++b) r.push_back(b < wdt ? fslot[entry(L[a], L[j0 + b])] : 0);
-        push(std::move(r));
+    const int32_t e_pp = entry(p, p);
+    const int32_t flags = (first[e_pp] < 0 ? 1 : 0) | (fused ? 0 : 2);
+    std::vector<int32_t> r = {(int32_t)((kRecPivot << 28) | (uint32_t)c), p,
+                              (int32_t)(bd.size() - qd), (int32_t)(bo.size() - qo), flags, ws};
+    std::vector<std::pair<int32_t, int32_t>> pt;
+    imm(r, pt, -1 - p);
+    operand(r, pt, p, p);
+    while (qd < bd.size()) birth(r, pt, bd[qd++]);
+    while (qo < bo.size()) birth(r, pt, bo[qo++]);
+    for (int32_t k = 0; k < c; ++k) operand(r, pt, L[k], p);
+    for (int32_t k = 0; k < c; ++k) operand(r, pt, p, L[k]);
+    auto row = [&](std::vector<int32_t>& out, int32_t a) {
+      for (int32_t b = 0; b < ws; ++b) out.push_back(b < c ? fslot[entry(L[a], L[b])] : 0);
+    };
+    if (fused)
+      for (int32_t a = 0; a < c; ++a) row(r, a);
+    push(std::move(r), std::move(pt));
+    if (!fused) {
+      const int32_t rows_per = std::max<int32_t>(1, (int32_t)((kMaxRec - 8) / ws));
+      for (int32_t a0 = 0; a0 < c; a0 += rows_per) {
+        const int32_t na = std::min(rows_per, c - a0);
+        std::vector<int32_t> u = {(int32_t)((kRecUpdate << 28) | (uint32_t)c), a0, na, ws, 0, 0, 0, 0};
+        for (int32_t a = a0; a < a0 + na; ++a) row(u, a);
+        push(std::move(u), {});
       }
     }
   }
-  push({(int32_t)(kRecEnd << 28), 0, 0, 0});
-  pack_chunks(recs, max_rec, P.f_chunk_words, P.f_stream);
+  push({(int32_t)(kRecEnd << 28), 0, 0, 0}, {});
+  pack_chunks(recs, max_rec, P.f_chunk_words, P.f_stream, &rec_patch, &P.f_patch_pos,
+              &P.f_patch_src);
 
   // ---------------- solve program ----------------
   // Forward substitution (column-oriented, pivots ascending):

@@ -24,6 +24,9 @@ struct HostPlan {
   // record streams packed in chunks
   int32_t f_slots = 0, f_births = 0, f_chunk_words = 0;
   std::vector<int32_t> f_stream;
+  // immediates of the factor stream: word position of each 64-bit cell and its source
+  // (>= 0: A index, nnz_A = structural zero; < 0: d[-1 - src], permuted numbering)
+  std::vector<int32_t> f_patch_pos, f_patch_src;
   int32_t y_slots = 0, x_slots = 0, s_chunk_words = 0;
   std::vector<int32_t> s_stream;
 };

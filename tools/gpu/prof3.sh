@@ -1,0 +1,5 @@
+timeout 300 python tools/gpu/diag.py --reps 3 --groups 1,2,4,8
+for G in 4; do
+ncu --set full --clock-control none --import-source on -k regex:factor_kernel -s 1 -c 1 \
+  -o gpurun_out/factor_G$G -f python tools/gpu/diag.py --groups $G --reps 1 --ladders 4096 > gpurun_out/ncu_f$G.log 2>&1; echo f$G=$?
+done
