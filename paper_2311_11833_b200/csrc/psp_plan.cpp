@@ -396,8 +396,8 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
   // ---------------- solve program ----------------
   // Forward substitution (column-oriented, pivots ascending):
   //   YBIRTH [1<<28 | nb, 0, 0, 0] + nb x (slot, original row): pending y_i <- b[row]
-  //   YPIVOT [2<<28 | c, ys, lofs, 0] + c target slots: y_j final (slot ys, or b if
-  //          never updated); y_i = fma(-l_ij, y_j, y_i) for the c rows of L(:, j)
+  //   YPIVOT [2<<28 | c, ys, lofs, perm[j]] + c target slots: y_j final (slot ys, or
+  //          b[perm[j]] if never updated); y_i = fma(-l_ij, y_j, y_i) for the c rows of L(:, j)
   //   YEND   [5<<28, 0, 0, 0]
   // Backward substitution (row-oriented, pivots descending, the sum in descending
   // column order, the division last):
@@ -436,7 +436,7 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
         spush(std::move(r));
       }
       std::vector<int32_t> r = {(int32_t)((kRecPivot << 28) | (uint32_t)lcol[j].size()),
-                                yb[j] >= 0 ? ys[j] : -1, P.lofs[j], 0};
+                                yb[j] >= 0 ? ys[j] : -1, P.lofs[j], perm[j]};
       for (int32_t i : lcol[j]) r.push_back(ys[i]);
       spush(std::move(r));
     }

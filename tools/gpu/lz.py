@@ -21,7 +21,6 @@ for ci in (0, 1):
             sv.psp_solve_batch(torch.tensor(s.b.T.copy(), dtype=torch.float64, device="cuda"))
             X = sv.psp_get_solutions().cpu().numpy()
             rc, st = sv.psp_get_lane_status()
-            d = np.abs(X - Xo).max(axis=(1, 2))
-            bad = np.argwhere(np.abs(X - Xo)[0, 0] > 0).ravel()
-            print(ci, lz, G, rc, st.tolist()[:8], d.tolist()[:8], "first bad idx", bad[:10].tolist(), flush=True)
+            badl = [k for k in range(len(eps)) if not np.array_equal(X[k], Xo[k])]
+            print(ci, lz, G, rc, "bitwise" if not badl else f"MISMATCH lanes {badl[:8]}", flush=True)
             sv.close()
