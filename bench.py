@@ -282,6 +282,10 @@ def main():
             if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
         peak = peaks.get("hbm_gbs", 6650.0)
         peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+        traffic = None   # ncu DRAM bytes per factor launch (profiles/), same workload only
+        tp = os.path.join(ROOT, "profiles", "r1_traffic.json")
+        if os.path.exists(tp) and K == 65536 and s.n == 531:
+            traffic = json.load(open(tp)).get("traffic_bytes_per_launch")
         kern = {"factor": (t_factor, bytes_factor), "solve": (t_solve, bytes_solve),
                 "recover": (t_recover, bytes_recover)}
         dom = max(kern, key=lambda k: kern[k][0])
@@ -306,7 +310,7 @@ def main():
                           "symbolic_once": 1e3 * t_sym},
             "hbm_gbs_algorithmic": (bytes_factor + bytes_solve + bytes_recover) / (ms_step * 1e-3) / 1e9,
             "roofline": {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak,
-                         "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": bdom, "launch_ms": tdom},
             "gpu_launches": 4 * args.steps,
