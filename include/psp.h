@@ -82,8 +82,10 @@ typedef struct {
                                     updated entries of the right-looking factorisation */
   int32_t solve_live;            /* live slots per lane of the triangular solves     */
   int32_t births;                /* pending-slot initialisations per lane            */
-  int32_t factor_groups;         /* G: thread groups sharing one slab of 32/G lanes in
-                                    the factor kernel                 */
+  int32_t factor_groups;         /* G: thread groups sharing one slab in the factor
+                                    kernel                            */
+  int32_t factor_lanes_per_thread; /* J: adjacent lanes per thread; a slab holds
+                                    32/G*J lanes                                     */
   int32_t factor_warps_per_cta;  /* consumer warps per factor CTA                    */
   int32_t factor_pend_smem;      /* 1: pending slots in shared memory, 0: global     */
   int32_t solve_live_smem;       /* 1: solve's live slots in shared memory, 0: global */
@@ -102,13 +104,15 @@ psp_status psp_create(psp_handle* out, int32_t device, void* cuda_stream);
 psp_status psp_destroy(psp_handle h);
 
 /* Options (set before psp_symbolic_analyse; they apply to the next analysis):
- *  PSP_OPT_FACTOR_GROUPS  0 (default): automatic; else G in {1, 2, 4, 8}: the factor
- *                         kernel splits each warp into G groups sharing one slab of
- *                         32/G lanes.  Results are bitwise independent of G.
+ *  PSP_OPT_FACTOR_GROUPS  0 (default): automatic; else G in {1, 2, 4}: the factor kernel
+ *                         splits each warp into G groups sharing one slab.
+ *  PSP_OPT_FACTOR_LANES   0 (default): automatic; else J in {1, 2} adjacent lanes per
+ *                         thread (J <= G); a slab holds 32/G*J lanes.
+ *                         Results are bitwise independent of G and J.
  *  PSP_OPT_FACTOR_WARPS   0 (default): automatic; else consumer warps per factor CTA
  *                         (1..16, capped by shared memory).
  * Errors: ARG. */
-enum { PSP_OPT_FACTOR_GROUPS = 1, PSP_OPT_FACTOR_WARPS = 2 };
+enum { PSP_OPT_FACTOR_GROUPS = 1, PSP_OPT_FACTOR_WARPS = 2, PSP_OPT_FACTOR_LANES = 3 };
 psp_status psp_set_option(psp_handle h, int32_t option, int64_t value);
 
 /* Rebind the handle to another stream of the same device. */

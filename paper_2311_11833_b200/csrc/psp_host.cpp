@@ -50,7 +50,7 @@ struct psp_ctx {
   std::vector<DevBuf> plan_bufs;
   DevicePlan plan;
   psp::LaunchInfo launch;
-  int64_t opt_groups = 0, opt_warps = 0;   // PSP_OPT_FACTOR_GROUPS / _WARPS (0 = automatic)
+  int64_t opt_groups = 0, opt_warps = 0, opt_lanes = 0;   // PSP_OPT_FACTOR_* (0 = automatic)
   DevBuf fscratch_d, sscratch_d;   // global pending buffers when shared memory is too small
 
   // --- perturbations ---
@@ -211,9 +211,14 @@ psp_status psp_set_option(psp_handle h, int32_t option, int64_t value) {
   if (!h) return PSP_ERR_ARG;
   switch (option) {
     case PSP_OPT_FACTOR_GROUPS:
-      if (value != 0 && value != 1 && value != 2 && value != 4 && value != 8)
-        return fail(h, PSP_ERR_ARG, "PSP_OPT_FACTOR_GROUPS must be 0, 1, 2, 4 or 8");
+      if (value != 0 && value != 1 && value != 2 && value != 4)
+        return fail(h, PSP_ERR_ARG, "PSP_OPT_FACTOR_GROUPS must be 0, 1, 2 or 4");
       h->opt_groups = value;
+      return PSP_OK;
+    case PSP_OPT_FACTOR_LANES:
+      if (value != 0 && value != 1 && value != 2)
+        return fail(h, PSP_ERR_ARG, "PSP_OPT_FACTOR_LANES must be 0, 1 or 2");
+      h->opt_lanes = value;
       return PSP_OK;
     case PSP_OPT_FACTOR_WARPS:
       if (value < 0 || value > psp::kMaxWarpsCta)
@@ -374,12 +379,14 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
   UP(acsc_ptr, acsc_ptr);
   UP(acsc_q, acsc_q);
 #undef UP
-  if (!psp::choose_launch(P, h->launch, (int)h->opt_groups, (int)h->opt_warps))
+  if (!psp::choose_launch(P, h->launch, (int)h->opt_groups, (int)h->opt_warps,
+                          (int)h->opt_lanes))
     return fail(h, PSP_ERR_UNSUPPORTED, "no kernel configuration fits shared memory "
                 "(program chunk %d words, c_max %d, solve live slots %d)", P.f_chunk_words,
                 P.c_max, P.y_slots + P.x_slots);
   if (!host_only)
-    CUDA_TRY(h, psp::configure_kernels(P, h->launch, (int)h->opt_groups, (int)h->opt_warps));
+    CUDA_TRY(h, psp::configure_kernels(P, h->launch, (int)h->opt_groups, (int)h->opt_warps,
+                                        (int)h->opt_lanes));
   h->plan = P;
   h->perm = perm;
   h->n = n;
@@ -413,6 +420,7 @@ psp_status psp_get_symbolic_info(psp_handle h, psp_symbolic_info* info, int32_t*
   info->solve_fma = h->solve_fma;
   info->max_live = h->max_live;
   info->factor_groups = h->launch.f_groups;
+  info->factor_lanes_per_thread = h->launch.f_lanes;
   info->factor_warps_per_cta = h->launch.f_warps;
   info->factor_pend_smem = h->launch.f_pend_smem ? 1 : 0;
   info->solve_live_smem = h->launch.s_live_smem ? 1 : 0;
@@ -521,7 +529,7 @@ psp_status psp_get_factor(psp_handle h, int32_t k, double* vals_h) {
   if (!h || !vals_h) return PSP_ERR_ARG;
   if (!h->factored) return fail(h, PSP_ERR_STATE, "factor_batch first");
   if (k < 0 || k >= h->K) return fail(h, PSP_ERR_ARG, "lane %d out of range", k);
-  const int L = kBlock / h->launch.f_groups;
+  const int L = kBlock / h->launch.f_groups * h->launch.f_lanes;
   const double* src = (const double*)h->V_d.p + (size_t)(k / L) * h->nnz_LU * L + (k % L);
   CUDA_TRY(h, cudaMemcpy2DAsync(vals_h, sizeof(double), src, sizeof(double) * L, sizeof(double),
                                 (size_t)h->nnz_LU, cudaMemcpyDeviceToHost, h->stream));

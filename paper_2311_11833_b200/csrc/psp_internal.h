@@ -47,7 +47,8 @@ struct DevicePlan {
 // Launch configuration chosen per plan (host, psp_kernels.cu: choose_launch).
 struct LaunchInfo {
   // factor
-  int f_groups = 1;            // G: thread groups per warp (L = 32 / G lanes per slab)
+  int f_groups = 1;            // G: thread groups per warp
+  int f_lanes = 1;             // J: lanes per thread; a slab has LS = 32 / G * J lanes
   bool f_pend_smem = false;    // pending slots in shared memory (else global scratch)
   int f_warps = 1;             // consumer warps (slabs) per CTA
   int f_smem = 0;              // dynamic shared memory per CTA
@@ -65,9 +66,10 @@ struct LaunchInfo {
 // force_groups: 0 = automatic, else G in {1, 2, 4, 8}; force_warps: 0 = automatic.
 // Returns false when no configuration fits the shared memory (the program's records or
 // the solve's working set are too large).
-bool choose_launch(const DevicePlan& p, LaunchInfo& li, int force_groups, int force_warps);
+bool choose_launch(const DevicePlan& p, LaunchInfo& li, int force_groups, int force_warps,
+                   int force_lanes);
 cudaError_t configure_kernels(const DevicePlan& p, LaunchInfo& li, int force_groups,
-                              int force_warps);
+                              int force_warps, int force_lanes);
 // Fill the factor stream's immediates (A values, d) in `stream_out` (device copy).
 cudaError_t launch_patch_program(const DevicePlan& p, int32_t* stream_out, const double* A_vals,
                                  const double* dperm, cudaStream_t stream);

@@ -23,7 +23,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ladders", type=int, default=8192)
     ap.add_argument("--grid", type=int, default=300)
-    ap.add_argument("--groups", default="0,1,2,4,8")
+    ap.add_argument("--groups", default="0,1:1,2:2,2:1,4:2", help="G:J pairs")
     ap.add_argument("--warps", type=int, default=0)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--R", type=int, default=1)
@@ -37,15 +37,17 @@ def main():
     A = torch.tensor(s.vals, dtype=torch.float64, device="cuda")
     B = torch.tensor(s.b.T.copy(), dtype=torch.float64, device="cuda")
     ref = None
-    for v in [int(x) for x in a.groups.split(",")]:
+    for gj in a.groups.split(","):
+        v, J = (int(x) for x in (gj + ":0").split(":")[:2])
         sv = psp.Solver(0)
         sv.psp_set_option("factor_groups", v)
+        sv.psp_set_option("factor_lanes", J)
         sv.psp_set_option("factor_warps", a.warps)
         t0 = time.perf_counter()
         sv.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, "mindeg")
         t_an = time.perf_counter() - t0
         info, _ = sv.psp_get_symbolic_info()
-        print(f"[groups={v}] analyse {t_an:.2f}s G={info['factor_groups']} warps/cta={info['factor_warps_per_cta']}"
+        print(f"[{gj}] analyse {t_an:.2f}s G={info['factor_groups']} J={info['factor_lanes_per_thread']} warps/cta={info['factor_warps_per_cta']}"
               f" pend_smem={info['factor_pend_smem']} solve_live_smem={info['solve_live_smem']}"
               f" nnz_LU={info['nnz_LU']} fma={info['factor_fma']} max_live={info['max_live']}", flush=True)
         sv.psp_set_perturbations(eps, s.d)
