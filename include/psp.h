@@ -86,6 +86,7 @@ typedef struct {
                                     kernel                            */
   int32_t factor_lanes_per_thread; /* J: adjacent lanes per thread; a slab holds
                                     32/G*J lanes                                     */
+  int32_t factor_slab_warps;     /* P: warps sharing one slab (rows split)          */
   int32_t factor_warps_per_cta;  /* consumer warps per factor CTA                    */
   int32_t factor_pend_smem;      /* 1: pending slots in shared memory, 0: global     */
   int32_t solve_live_smem;       /* 1: solve's live slots in shared memory, 0: global */
@@ -109,10 +110,13 @@ psp_status psp_destroy(psp_handle h);
  *  PSP_OPT_FACTOR_LANES   0 (default): automatic; else J in {1, 2} adjacent lanes per
  *                         thread (J <= G); a slab holds 32/G*J lanes.
  *                         Results are bitwise independent of G and J.
+ *  PSP_OPT_FACTOR_SLAB_WARPS 0 (default): automatic; else P in {1, 2} warps sharing one
+ *                         slab (G = J = 1 only), the rows of each pivot split between them.
  *  PSP_OPT_FACTOR_WARPS   0 (default): automatic; else consumer warps per factor CTA
  *                         (1..16, capped by shared memory).
  * Errors: ARG. */
-enum { PSP_OPT_FACTOR_GROUPS = 1, PSP_OPT_FACTOR_WARPS = 2, PSP_OPT_FACTOR_LANES = 3 };
+enum { PSP_OPT_FACTOR_GROUPS = 1, PSP_OPT_FACTOR_WARPS = 2, PSP_OPT_FACTOR_LANES = 3,
+       PSP_OPT_FACTOR_SLAB_WARPS = 4 };
 psp_status psp_set_option(psp_handle h, int32_t option, int64_t value);
 
 /* Rebind the handle to another stream of the same device. */

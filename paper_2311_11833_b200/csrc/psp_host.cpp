@@ -50,7 +50,7 @@ struct psp_ctx {
   std::vector<DevBuf> plan_bufs;
   DevicePlan plan;
   psp::LaunchInfo launch;
-  int64_t opt_groups = 0, opt_warps = 0, opt_lanes = 0;   // PSP_OPT_FACTOR_* (0 = automatic)
+  int64_t opt_groups = 0, opt_warps = 0, opt_lanes = 0, opt_slab_warps = 0;  // PSP_OPT_FACTOR_*
   DevBuf fscratch_d, sscratch_d;   // global pending buffers when shared memory is too small
 
   // --- perturbations ---
@@ -220,6 +220,11 @@ psp_status psp_set_option(psp_handle h, int32_t option, int64_t value) {
         return fail(h, PSP_ERR_ARG, "PSP_OPT_FACTOR_LANES must be 0, 1 or 2");
       h->opt_lanes = value;
       return PSP_OK;
+    case PSP_OPT_FACTOR_SLAB_WARPS:
+      if (value != 0 && value != 1 && value != 2)
+        return fail(h, PSP_ERR_ARG, "PSP_OPT_FACTOR_SLAB_WARPS must be 0, 1 or 2");
+      h->opt_slab_warps = value;
+      return PSP_OK;
     case PSP_OPT_FACTOR_WARPS:
       if (value < 0 || value > psp::kMaxWarpsCta)
         return fail(h, PSP_ERR_ARG, "PSP_OPT_FACTOR_WARPS must be in [0, %d]", psp::kMaxWarpsCta);
@@ -367,6 +372,9 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
   P.x_slots = HP.x_slots;
   P.s_chunk_words = HP.s_chunk_words;
   P.s_nchunks = (int32_t)(HP.s_stream.size() / HP.s_chunk_words);
+  P.s_rows = HP.s_rows;
+  P.s_nfwd = HP.s_nfwd;
+  P.s_nfc = (int32_t)HP.s_fchunks.size() / 2;
   psp_status s;
 #define UP(vec, field) \
   if (!host_only && (s = upload(h, vec, &P.field))) return s;
@@ -376,17 +384,22 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
   UP(HP.f_patch_pos, f_patch_pos);
   UP(HP.f_patch_src, f_patch_src);
   UP(HP.s_stream, s_stream);
+  if (!host_only) {
+    const int32_t* fc = nullptr;
+    if ((s = upload(h, HP.s_fchunks, &fc))) return s;
+    P.s_fchunks = reinterpret_cast<const int2*>(fc);
+  }
   UP(acsc_ptr, acsc_ptr);
   UP(acsc_q, acsc_q);
 #undef UP
   if (!psp::choose_launch(P, h->launch, (int)h->opt_groups, (int)h->opt_warps,
-                          (int)h->opt_lanes))
+                          (int)h->opt_lanes, (int)h->opt_slab_warps))
     return fail(h, PSP_ERR_UNSUPPORTED, "no kernel configuration fits shared memory "
                 "(program chunk %d words, c_max %d, solve live slots %d)", P.f_chunk_words,
                 P.c_max, P.y_slots + P.x_slots);
   if (!host_only)
     CUDA_TRY(h, psp::configure_kernels(P, h->launch, (int)h->opt_groups, (int)h->opt_warps,
-                                        (int)h->opt_lanes));
+                                        (int)h->opt_lanes, (int)h->opt_slab_warps));
   h->plan = P;
   h->perm = perm;
   h->n = n;
@@ -421,6 +434,7 @@ psp_status psp_get_symbolic_info(psp_handle h, psp_symbolic_info* info, int32_t*
   info->max_live = h->max_live;
   info->factor_groups = h->launch.f_groups;
   info->factor_lanes_per_thread = h->launch.f_lanes;
+  info->factor_slab_warps = h->launch.f_slab_warps;
   info->factor_warps_per_cta = h->launch.f_warps;
   info->factor_pend_smem = h->launch.f_pend_smem ? 1 : 0;
   info->solve_live_smem = h->launch.s_live_smem ? 1 : 0;

@@ -18,7 +18,7 @@ constexpr int kBlock = 32;
 // extended by one structural zero, A[nnz_A] = 0.
 constexpr int kStages = 4;            // depth of the CTA-shared program ring
 constexpr int kDataStages = 3;        // depth of the solve's per-warp factor-row ring
-constexpr int kDataRows = 16;         // factor rows per stage of that ring
+constexpr int kSolveMaxC = 16;        // records with c <= kSolveMaxC take the unrolled path
 constexpr int kMaxWarpsCta = 16;      // consumer warps per CTA (plus one producer warp)
 constexpr int kFusedMax = 16;         // pivots with c <= kFusedMax: u in registers, no scratch
 
@@ -39,6 +39,8 @@ struct DevicePlan {
   // solve program: forward (ascending) records, YEND, backward (descending) records, END
   int32_t y_slots = 0, x_slots = 0, s_chunk_words = 0, s_nchunks = 0;
   const int32_t* s_stream = nullptr;
+  int32_t s_rows = 16, s_nfwd = 0, s_nfc = 0;   // ring stage rows; forward / all row chunks
+  const int2* s_fchunks = nullptr;              // [s_nfc] row ranges [r0, r1)
   // deterministic column sums for the default pivot tolerance
   const int32_t* acsc_ptr = nullptr;   // [n+1]
   const int32_t* acsc_q = nullptr;     // [nnz_A]
@@ -49,8 +51,9 @@ struct LaunchInfo {
   // factor
   int f_groups = 1;            // G: thread groups per warp
   int f_lanes = 1;             // J: lanes per thread; a slab has LS = 32 / G * J lanes
+  int f_slab_warps = 1;        // P: warps sharing one slab (rows split, named barriers)
   bool f_pend_smem = false;    // pending slots in shared memory (else global scratch)
-  int f_warps = 1;             // consumer warps (slabs) per CTA
+  int f_warps = 1;             // consumer warps per CTA (f_warps / P slabs)
   int f_smem = 0;              // dynamic shared memory per CTA
   int f_off_warp = 0, f_warp_bytes = 0, f_off_scr = 0;
   int f_ctas_per_sm = 0;
@@ -67,9 +70,9 @@ struct LaunchInfo {
 // Returns false when no configuration fits the shared memory (the program's records or
 // the solve's working set are too large).
 bool choose_launch(const DevicePlan& p, LaunchInfo& li, int force_groups, int force_warps,
-                   int force_lanes);
+                   int force_lanes, int force_slab_warps);
 cudaError_t configure_kernels(const DevicePlan& p, LaunchInfo& li, int force_groups,
-                              int force_warps, int force_lanes);
+                              int force_warps, int force_lanes, int force_slab_warps);
 // Fill the factor stream's immediates (A values, d) in `stream_out` (device copy).
 cudaError_t launch_patch_program(const DevicePlan& p, int32_t* stream_out, const double* A_vals,
                                  const double* dperm, cudaStream_t stream);

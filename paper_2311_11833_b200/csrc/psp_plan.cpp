@@ -462,6 +462,37 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
     spush({(int32_t)(kRecEnd << 28), 0, 0, 0});
   }
   pack_chunks(srec, smax, P.s_chunk_words, P.s_stream);
+
+  // Factor-row chunks of the solve, in consumption order: the L region ascending
+  // (forward), then the DU region descending (backward).  A chunk holds <= s_rows rows
+  // and never splits the rows one record consumes (a pivot's c rows of L; a row's 1 + c
+  // rows of DU), so the kernel checks the ring once per record, not per element.
+  P.s_rows = std::max<int32_t>(16, (P.c_max + 2) & ~1);
+  P.s_fchunks.clear();
+  {
+    int32_t r0 = 0, r1 = 0;
+    for (int32_t j = 0; j < n; ++j) {
+      const int32_t c = P.lofs[j + 1] - P.lofs[j];
+      if (c == 0) continue;
+      if (P.lofs[j + 1] - r0 > P.s_rows) {
+        P.s_fchunks.insert(P.s_fchunks.end(), {r0, r1});
+        r0 = P.lofs[j];
+      }
+      r1 = P.lofs[j + 1];
+    }
+    if (r1 > r0) P.s_fchunks.insert(P.s_fchunks.end(), {r0, r1});
+    P.s_nfwd = (int32_t)P.s_fchunks.size() / 2;
+    int32_t hi = P.nnz_LU, lo = P.nnz_LU;
+    for (int32_t i = n - 1; i >= 0; --i) {
+      const int32_t b0 = P.nnz_L + P.dofs[i];
+      if (hi - b0 > P.s_rows) {
+        P.s_fchunks.insert(P.s_fchunks.end(), {lo, hi});
+        hi = lo;
+      }
+      lo = b0;
+    }
+    P.s_fchunks.insert(P.s_fchunks.end(), {lo, hi});
+  }
 }
 
 }  // namespace psp

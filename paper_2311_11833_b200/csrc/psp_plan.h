@@ -29,6 +29,10 @@ struct HostPlan {
   std::vector<int32_t> f_patch_pos, f_patch_src;
   int32_t y_slots = 0, x_slots = 0, s_chunk_words = 0;
   std::vector<int32_t> s_stream;
+  // factor-row chunks of the solve (pairs r0, r1 in consumption order; the first s_nfwd
+  // are the forward pass's), at most s_rows rows each
+  int32_t s_rows = 16, s_nfwd = 0;
+  std::vector<int32_t> s_fchunks;
 };
 
 std::vector<int32_t> min_degree_order(int32_t n, const std::vector<std::vector<int32_t>>& adj,

@@ -25,7 +25,7 @@ EXPORTS = ["psp_create", "psp_destroy", "psp_set_stream", "psp_status_string",
            "psp_set_perturbations", "psp_factor_batch", "psp_solve_batch", "psp_get_solutions",
            "psp_set_weights", "psp_recover", "psp_get_lane_status", "psp_solve_host",
            "psp_synchronize", "psp_ladder_weights", "psp_set_option", "psp_get_factor"]
-OPT = {"factor_groups": 1, "factor_warps": 2, "factor_lanes": 3}
+OPT = {"factor_groups": 1, "factor_warps": 2, "factor_lanes": 3, "factor_slab_warps": 4}
 
 
 class SymbolicInfo(ctypes.Structure):
@@ -35,7 +35,7 @@ class SymbolicInfo(ctypes.Structure):
                 ("factor_div", ctypes.c_int64), ("solve_fma", ctypes.c_int64),
                 ("max_live", ctypes.c_int32), ("solve_live", ctypes.c_int32),
                 ("births", ctypes.c_int32), ("factor_groups", ctypes.c_int32),
-                ("factor_lanes_per_thread", ctypes.c_int32),
+                ("factor_lanes_per_thread", ctypes.c_int32), ("factor_slab_warps", ctypes.c_int32),
                 ("factor_warps_per_cta", ctypes.c_int32), ("factor_pend_smem", ctypes.c_int32),
                 ("solve_live_smem", ctypes.c_int32)]
 

@@ -38,16 +38,17 @@ def main():
     B = torch.tensor(s.b.T.copy(), dtype=torch.float64, device="cuda")
     ref = None
     for gj in a.groups.split(","):
-        v, J = (int(x) for x in (gj + ":0").split(":")[:2])
+        v, J, P = (int(x) for x in (gj + ":0:0").split(":")[:3])
         sv = psp.Solver(0)
         sv.psp_set_option("factor_groups", v)
         sv.psp_set_option("factor_lanes", J)
+        sv.psp_set_option("factor_slab_warps", P)
         sv.psp_set_option("factor_warps", a.warps)
         t0 = time.perf_counter()
         sv.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, "mindeg")
         t_an = time.perf_counter() - t0
         info, _ = sv.psp_get_symbolic_info()
-        print(f"[{gj}] analyse {t_an:.2f}s G={info['factor_groups']} J={info['factor_lanes_per_thread']} warps/cta={info['factor_warps_per_cta']}"
+        print(f"[{gj}] analyse {t_an:.2f}s G={info['factor_groups']} J={info['factor_lanes_per_thread']} P={info['factor_slab_warps']} warps/cta={info['factor_warps_per_cta']}"
               f" pend_smem={info['factor_pend_smem']} solve_live_smem={info['solve_live_smem']}"
               f" nnz_LU={info['nnz_LU']} fma={info['factor_fma']} max_live={info['max_live']}", flush=True)
         sv.psp_set_perturbations(eps, s.d)
