@@ -53,23 +53,34 @@ def _json_print(d):
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+    """nvidia-smi clocks/throttle reasons sampled every 20 ms from before the warm-up
+    until after the timed region; samples are kept when their timestamp falls inside
+    the timed region (`mark_start` / `mark_end`), else (a very short region) the samples
+    of the whole loaded run are reported and labelled so."""
+    Q = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu_index):
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.t0 = self.t1 = None
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                       "--format=csv,noheader,nounits", "-lms", "20"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
 
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+
     def stop(self):
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.05)
         self.p.terminate()
         try:
             self.p.wait(timeout=5)
@@ -80,15 +91,25 @@ class ClockSampler:
         with open(self.f.name) as fh:
             for line in fh:
                 parts = [x.strip() for x in line.split(",")]
-                if len(parts) >= 7:
-                    rows.append(parts)
+                if len(parts) >= 8:
+                    try:
+                        ts = time.mktime(time.strptime(parts[0].split(".")[0], "%Y/%m/%d %H:%M:%S"))
+                        ts += float("0." + parts[0].split(".")[1]) if "." in parts[0] else 0.0
+                    except Exception:
+                        ts = None
+                    rows.append((ts, parts[1:]))
         os.unlink(self.f.name)
-        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        inside = [r for ts, r in rows if ts is not None and self.t0 is not None
+                  and self.t0 - 0.02 <= ts <= self.t1 + 0.02]
+        window = "timed region" if inside else "warm-up + timed region"
+        use = inside if inside else [r for _, r in rows]
+        sm = [float(r[0]) for r in use if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in use if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i] == "Active"})
+        reasons = sorted({names[i] for r in use for i in range(4) if r[3 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(use),
+                "window": window}
 
 
 def oracle_lanes(s, perm, eps, tol, threads=None):
@@ -221,6 +242,7 @@ def main():
         if ev is not None:
             ev[3].record(stream)
 
+    clk = ClockSampler(local_rank) if rank == 0 else None
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -228,10 +250,11 @@ def main():
     n_failed = int((st != 0).sum())
 
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
-    clk = ClockSampler(local_rank) if rank == 0 else None
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    if clk:
+        clk.mark_start()
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
     start.record(stream)
@@ -239,6 +262,8 @@ def main():
         step(evs[i])
     end.record(stream)
     torch.cuda.synchronize()
+    if clk:
+        clk.mark_end()
     if world > 1:
         dist.barrier()
     clocks = clk.stop() if clk else None

@@ -52,6 +52,7 @@ struct psp_ctx {
   psp::LaunchInfo launch;
   int64_t opt_groups = 0, opt_warps = 0, opt_lanes = 0, opt_slab_warps = 0;  // PSP_OPT_FACTOR_*
   DevBuf fscratch_d, sscratch_d;   // global pending buffers when shared memory is too small
+  DevBuf fscr_d;                   // global l/u scratch rows (large pivots) when needed
 
   // --- perturbations ---
   int32_t K = 0, K_pad = 0;
@@ -136,6 +137,7 @@ static void reset_numeric(psp_ctx* h) {
   h->status_d.release();
   h->X_d.release();
   h->fscratch_d.release();
+  h->fscr_d.release();
   h->sscratch_d.release();
   h->wptr_d.release();
   h->wlane_d.release();
@@ -494,9 +496,18 @@ psp_status psp_factor_batch(psp_handle h, const double* A_vals, double pivot_tol
   }
   CUDA_TRY(h, psp::launch_patch_program(h->plan, const_cast<int32_t*>(h->plan.f_stream), A_vals,
                                         (const double*)h->dperm_d.p, h->stream));
+  if (!h->launch.f_scr_smem) {
+    psp_status s;
+    size_t need = sizeof(double) * (size_t)h->K_pad * 2 * h->plan.c_scr;
+    if (h->fscr_d.bytes < need) {
+      CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+      if ((s = ensure(h, h->fscr_d, need))) return s;
+    }
+  }
   CUDA_TRY(h, psp::launch_factor(h->plan, h->launch, h->plan.f_stream, (const double*)h->eps_d.p,
                                  tol_dev, pivot_tol, (double*)h->V_d.p, (double*)h->fscratch_d.p,
-                                 (int32_t*)h->status_d.p, h->K_pad, h->stream));
+                                 (double*)h->fscr_d.p, (int32_t*)h->status_d.p, h->K_pad,
+                                 h->stream));
   if (lane_status)
     CUDA_TRY(h, cudaMemcpyAsync(lane_status, h->status_d.p, sizeof(int32_t) * h->K,
                                 cudaMemcpyDeviceToDevice, h->stream));

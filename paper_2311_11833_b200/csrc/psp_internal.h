@@ -53,12 +53,14 @@ struct LaunchInfo {
   int f_lanes = 1;             // J: lanes per thread; a slab has LS = 32 / G * J lanes
   int f_slab_warps = 1;        // P: warps sharing one slab (rows split, named barriers)
   bool f_pend_smem = false;    // pending slots in shared memory (else global scratch)
+  bool f_scr_smem = true;      // l/u scratch rows of large pivots in shared memory
   int f_warps = 1;             // consumer warps per CTA (f_warps / P slabs)
   int f_smem = 0;              // dynamic shared memory per CTA
   int f_off_warp = 0, f_warp_bytes = 0, f_off_scr = 0;
   int f_ctas_per_sm = 0;
   // solve
   bool s_live_smem = false;
+  bool s_b_smem = true;        // b staged in shared memory (else read from global)
   int s_warps = 1;
   int s_smem = 0;
   int s_off_b = 0, s_off_warp = 0, s_warp_bytes = 0, s_off_data = 0;
@@ -80,7 +82,8 @@ cudaError_t launch_pivot_tol(const DevicePlan& p, const double* A_vals, double* 
                              cudaStream_t stream);
 cudaError_t launch_factor(const DevicePlan& p, const LaunchInfo& li, const int32_t* prog,
                           const double* eps, const double* tol_dev, double tol_value, double* V,
-                          double* gscratch, int32_t* status, int32_t K_pad, cudaStream_t stream);
+                          double* gscratch, double* gscr, int32_t* status, int32_t K_pad,
+                          cudaStream_t stream);
 cudaError_t launch_solve(const DevicePlan& p, const LaunchInfo& li, const double* V,
                          const double* B, int64_t ldb, int32_t R, double* X, double* gscratch,
                          int32_t K_pad, cudaStream_t stream);

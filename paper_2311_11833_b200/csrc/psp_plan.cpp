@@ -467,27 +467,38 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
   // (forward), then the DU region descending (backward).  A chunk holds <= s_rows rows
   // and never splits the rows one record consumes (a pivot's c rows of L; a row's 1 + c
   // rows of DU), so the kernel checks the ring once per record, not per element.
-  P.s_rows = std::max<int32_t>(16, (P.c_max + 2) & ~1);
+  P.s_rows = std::min<int32_t>(32, std::max<int32_t>(16, (P.c_max + 2) & ~1));
   P.s_fchunks.clear();
   {
+    // (a record longer than s_rows is split across chunks; the kernel then reads it
+    // element by element)
+    const int32_t S = P.s_rows;
     int32_t r0 = 0, r1 = 0;
     for (int32_t j = 0; j < n; ++j) {
-      const int32_t c = P.lofs[j + 1] - P.lofs[j];
-      if (c == 0) continue;
-      if (P.lofs[j + 1] - r0 > P.s_rows) {
-        P.s_fchunks.insert(P.s_fchunks.end(), {r0, r1});
-        r0 = P.lofs[j];
+      const int32_t a = P.lofs[j], b = P.lofs[j + 1];
+      if (b == a) continue;
+      if (b - r0 > S) {
+        if (r1 > r0) P.s_fchunks.insert(P.s_fchunks.end(), {r0, r1});
+        r0 = a;
+        while (b - r0 > S) {
+          P.s_fchunks.insert(P.s_fchunks.end(), {r0, r0 + S});
+          r0 += S;
+        }
       }
-      r1 = P.lofs[j + 1];
+      r1 = b;
     }
     if (r1 > r0) P.s_fchunks.insert(P.s_fchunks.end(), {r0, r1});
     P.s_nfwd = (int32_t)P.s_fchunks.size() / 2;
     int32_t hi = P.nnz_LU, lo = P.nnz_LU;
     for (int32_t i = n - 1; i >= 0; --i) {
       const int32_t b0 = P.nnz_L + P.dofs[i];
-      if (hi - b0 > P.s_rows) {
-        P.s_fchunks.insert(P.s_fchunks.end(), {lo, hi});
+      if (hi - b0 > S) {
+        if (hi > lo) P.s_fchunks.insert(P.s_fchunks.end(), {lo, hi});
         hi = lo;
+        while (hi - b0 > S) {
+          P.s_fchunks.insert(P.s_fchunks.end(), {hi - S, hi});
+          hi -= S;
+        }
       }
       lo = b0;
     }

@@ -251,6 +251,27 @@ def ladder_weights_csr(ladders, lane_offset=0, k_begin=0, k_end=None):
     return np.array(ptr, np.int32), np.array(lane, np.int32), np.array(val, np.float64)
 
 
+def shard_range(K, rank, world):
+    """Contiguous lane shard [k_begin, k_end) of `rank` among `world` ranks (SURVEY
+    §8(e)): the K lanes split as evenly as possible, lower ranks first."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    base, extra = divmod(int(K), world)
+    k_begin = rank * base + min(rank, extra)
+    return k_begin, k_begin + base + (1 if rank < extra else 0)
+
+
+def recover_allreduce(solver, out, group=None):
+    """Row a5 + a6: this rank's partial sums x_hat[w] = sum over its lanes of w_k x_k
+    (psp_recover, on the device), then the sum over ranks (torch.distributed all-reduce:
+    NCCL over NVLink on GPUs).  With one rank (or no process group) it is psp_recover."""
+    solver.psp_recover(out)
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(out, op=dist.ReduceOp.SUM, group=group)
+    return out
+
+
 class HostSymbolic:
     """Host-only handle (psp_create with device = -1): symbolic analysis only."""
 

@@ -247,3 +247,66 @@ def test_diagonal_closed_form_at_full_size():
     pred *= r ** m * (b / a)
     err = (b / a) - g["xhat"][0, 0]
     assert np.max(np.abs(err - pred)) <= 16 * np.finfo(float).eps * np.max(np.abs(b / a))
+
+
+@pytest.mark.parametrize("gjp", [(1, 1, 1), (1, 1, 2), (2, 1, 1), (2, 2, 1), (4, 1, 1), (4, 2, 1)])
+def test_factor_kernel_variants_bitwise(gjp):
+    """Every warp/lane organisation of the factor kernel (G groups per warp, J lanes per
+    thread, P warps per slab) keeps the canonical order: lanes bitwise equal to the
+    oracle (leading-zero regime, growth ~1/eps, several slabs and a ragged tail)."""
+    G, J, P = gjp
+    s = config(1).system()
+    rng = np.random.default_rng(7)
+    K = 100
+    eps = rng.choice([-1, 1], K) * 10.0 ** rng.uniform(-6, -2, K)
+    solver = psp.Solver(0)
+    solver.psp_set_option("factor_groups", G)
+    solver.psp_set_option("factor_lanes", J)
+    solver.psp_set_option("factor_slab_warps", P)
+    solver.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering="mindeg_first", first_node=s.slot_p)
+    info, perm = solver.psp_get_symbolic_info()
+    assert (info["factor_groups"], info["factor_lanes_per_thread"], info["factor_slab_warps"]) == gjp
+    solver.psp_set_perturbations(eps, s.d)
+    solver.psp_factor_batch(torch.tensor(s.vals, dtype=torch.float64, device="cuda"), 1e-300)
+    solver.psp_solve_batch(torch.tensor(s.b.T.copy(), dtype=torch.float64, device="cuda"))
+    X = solver.psp_get_solutions().cpu().numpy()
+    Xo, sto = oracle.SparseOracle(s, perm).batch(eps, 1e-300)
+    assert np.array_equal(X, Xo)
+    # the factor itself, entry by entry, against a G=J=P=1 run
+    ref = psp.Solver(0)
+    ref.psp_set_option("factor_groups", 1)
+    ref.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering="mindeg_first", first_node=s.slot_p)
+    ref.psp_set_perturbations(eps, s.d)
+    ref.psp_factor_batch(torch.tensor(s.vals, dtype=torch.float64, device="cuda"), 1e-300)
+    for k in (0, 31, 32, 99):
+        assert np.array_equal(solver.psp_get_factor(k, info["nnz_LU"]), ref.psp_get_factor(k, info["nnz_LU"]))
+
+
+def test_sharded_recover_partials_sum_to_full():
+    """Row a6 on one GPU: lanes split over two handles (a ladder straddles the split);
+    each recovers its partial sums with its shard of the weights; their sum equals the
+    single-handle recovery up to the summation order (reading R16)."""
+    w = config(1, n_ladders=6)
+    s = w.system()
+    eps = w.eps()
+    K = len(eps)
+    A = torch.tensor(s.vals, dtype=torch.float64, device="cuda")
+    B = torch.tensor(s.b.T.copy(), dtype=torch.float64, device="cuda")
+
+    def run(kb, ke):
+        sv = psp.Solver(0)
+        sv.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering="mindeg")
+        sv.psp_set_perturbations(eps[kb:ke], s.d)
+        sv.psp_factor_batch(A, 0.0)
+        sv.psp_solve_batch(B)
+        sv.psp_set_weights(*psp.ladder_weights_csr(w.ladders, k_begin=kb, k_end=ke))
+        out = sv.psp_recover()
+        torch.cuda.synchronize()
+        return out.cpu().numpy()
+
+    full = run(0, K)
+    cut = K // 2 + 4                   # mid-ladder: lanes [0, cut) and [cut, K)
+    assert cut % 8 != 0
+    tot = run(0, cut) + run(cut, K)
+    scale = np.abs(full).max()
+    assert np.max(np.abs(tot - full)) <= 64 * np.finfo(float).eps * scale
