@@ -17,7 +17,8 @@ constexpr int kBlock = 32;
 // Source codes of the factor program: >= 0 pending slot; otherwise A[-1 - code] of A
 // extended by one structural zero, A[nnz_A] = 0.
 constexpr int kStages = 4;            // depth of the CTA-shared program ring
-constexpr int kDataStages = 3;        // depth of the solve's per-warp factor-row ring
+constexpr int kYRows = 16;            // y rows per stage of the solve's y ring
+constexpr int kDataStages = 2;        // depth of the solve's per-warp factor-row ring
 constexpr int kSolveMaxC = 16;        // records with c <= kSolveMaxC take the unrolled path
 constexpr int kMaxWarpsCta = 16;      // consumer warps per CTA (plus one producer warp)
 constexpr int kFusedMax = 16;         // pivots with c <= kFusedMax: u in registers, no scratch

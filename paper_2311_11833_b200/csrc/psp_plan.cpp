@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <climits>
 #include <functional>
+#include <cstdlib>
 #include <set>
 
 namespace psp {
@@ -468,6 +469,8 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
   // and never splits the rows one record consumes (a pivot's c rows of L; a row's 1 + c
   // rows of DU), so the kernel checks the ring once per record, not per element.
   P.s_rows = std::min<int32_t>(32, std::max<int32_t>(16, (P.c_max + 2) & ~1));
+  if (const char* env = std::getenv("PSP_SOLVE_ROWS"))   // tuning experiments only
+    P.s_rows = std::max<int32_t>((P.c_max + 2) & ~1, std::atoi(env));
   P.s_fchunks.clear();
   {
     // (a record longer than s_rows is split across chunks; the kernel then reads it
