@@ -67,6 +67,8 @@ struct psp_ctx {
   // --- weights ---
   int32_t W = 0;
   DevBuf wptr_d, wlane_d, wval_d, flag_d;
+  // fast combination layout (every row a contiguous run of <= 16 lanes in one 32-lane block)
+  bool w_seg = false;
   bool recovered = false;
 
   // --- host-API staging ---
@@ -142,6 +144,7 @@ static void reset_numeric(psp_ctx* h) {
   h->wptr_d.release();
   h->wlane_d.release();
   h->wval_d.release();
+  h->w_seg = false;
   h->K = h->K_pad = h->R = h->W = 0;
   h->factored = h->solved = h->recovered = false;
 }
@@ -381,6 +384,9 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
 #define UP(vec, field) \
   if (!host_only && (s = upload(h, vec, &P.field))) return s;
   UP(perm, perm);
+  std::vector<int32_t> iperm(n);
+  for (int32_t i = 0; i < n; ++i) iperm[perm[i]] = i;
+  UP(iperm, iperm);
   UP(HP.adiag, adiag);
   UP(HP.f_stream, f_stream);   // patched in place with A and d before every factorisation
   UP(HP.f_patch_pos, f_patch_pos);
@@ -596,6 +602,18 @@ psp_status psp_set_weights(psp_handle h, int32_t W, const int32_t* w_ptr_h,
     CUDA_TRY(h, cudaMemcpy(h->wlane_d.p, lane.data(), sizeof(int32_t) * lane.size(), cudaMemcpyHostToDevice));
     CUDA_TRY(h, cudaMemcpy(h->wval_d.p, val.data(), sizeof(double) * val.size(), cudaMemcpyHostToDevice));
   }
+  // fast-path detection (psp_kernels.cu recover_seg_kernel): every row a contiguous run
+  // of <= 16 lanes inside one 32-lane block
+  {
+    bool ok = true;
+    for (int32_t w = 0; w < W && ok; ++w) {
+      const int32_t q0 = ptr[w], q1 = ptr[w + 1];
+      if (q0 == q1) continue;
+      const int32_t k0 = lane[q0], k1 = lane[q1 - 1];
+      ok = k1 - k0 == q1 - q0 - 1 && k0 / kBlock == k1 / kBlock && q1 - q0 <= 16;
+    }
+    h->w_seg = ok;
+  }
   h->W = W;
   return PSP_OK;
 }
@@ -603,10 +621,17 @@ psp_status psp_set_weights(psp_handle h, int32_t W, const int32_t* w_ptr_h,
 psp_status psp_recover(psp_handle h, double* x) {
   if (!h || !x) return PSP_ERR_ARG;
   if (!h->solved || h->W == 0) return fail(h, PSP_ERR_STATE, "solve_batch and set_weights first");
-  CUDA_TRY(h, psp::launch_recover(h->plan, h->W, h->R, (const int32_t*)h->wptr_d.p,
-                                  (const int32_t*)h->wlane_d.p, (const double*)h->wval_d.p,
-                                  (const double*)h->X_d.p, (const int32_t*)h->status_d.p, x,
-                                  (int32_t*)h->flag_d.p, h->stream));
+  if (h->w_seg) {
+    CUDA_TRY(h, psp::launch_recover_seg(h->plan, h->W, h->R, (const int32_t*)h->wptr_d.p,
+                                        (const int32_t*)h->wlane_d.p, (const double*)h->wval_d.p,
+                                        (const double*)h->X_d.p, (const int32_t*)h->status_d.p, x,
+                                        (int32_t*)h->flag_d.p, h->stream));
+  } else {
+    CUDA_TRY(h, psp::launch_recover(h->plan, h->W, h->R, (const int32_t*)h->wptr_d.p,
+                                    (const int32_t*)h->wlane_d.p, (const double*)h->wval_d.p,
+                                    (const double*)h->X_d.p, (const int32_t*)h->status_d.p, x,
+                                    (int32_t*)h->flag_d.p, h->stream));
+  }
   h->recovered = true;
   return PSP_OK;
 }

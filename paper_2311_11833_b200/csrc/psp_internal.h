@@ -30,6 +30,7 @@ enum : uint32_t { kRecBirth = 1u, kRecPivot = 2u, kRecUpdate = 3u, kRecEnd = 4u,
 struct DevicePlan {
   int32_t n = 0, nnz_A = 0, nnz_LU = 0, nnz_L = 0, c_max = 0;
   const int32_t* perm = nullptr;       // [n]  perm[new] = old
+  const int32_t* iperm = nullptr;      // [n]  iperm[old] = new
   const int32_t* adiag = nullptr;      // [n]  CSR index of A(perm[i], perm[i]) or -1
   // factor program (records packed in chunks of f_chunk_words)
   int32_t f_slots = 0, f_chunk_words = 0, f_nchunks = 0, c_scr = 0;  // c_scr: scratch rows
@@ -92,6 +93,10 @@ cudaError_t launch_recover(const DevicePlan& p, int32_t W, int32_t R, const int3
                            const int32_t* w_lane, const double* w_val, const double* X,
                            const int32_t* status, double* x_out, int32_t* infeasible_flag,
                            cudaStream_t stream);
+cudaError_t launch_recover_seg(const DevicePlan& p, int32_t W, int32_t R, const int32_t* w_ptr,
+                               const int32_t* w_lane, const double* w_val, const double* X,
+                               const int32_t* status, double* x_out, int32_t* flag,
+                               cudaStream_t stream);
 cudaError_t launch_gather_solutions(const DevicePlan& p, int32_t K, int32_t R, const double* X,
                                     double* out, cudaStream_t stream);
 
