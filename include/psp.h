@@ -112,11 +112,13 @@ psp_status psp_destroy(psp_handle h);
  *                         Results are bitwise independent of G and J.
  *  PSP_OPT_FACTOR_SLAB_WARPS 0 (default): automatic; else P in {1, 2} warps sharing one
  *                         slab (G = J = 1 only), the rows of each pivot split between them.
+ *  PSP_OPT_FACTOR_PAIRS   1 (default): fuse supernode pivot pairs (p, p+1 with
+ *                         L(:,p) = {p+1} u L(:,p+1)) into one record; 0: off.
  *  PSP_OPT_FACTOR_WARPS   0 (default): automatic; else consumer warps per factor CTA
  *                         (1..16, capped by shared memory).
  * Errors: ARG. */
 enum { PSP_OPT_FACTOR_GROUPS = 1, PSP_OPT_FACTOR_WARPS = 2, PSP_OPT_FACTOR_LANES = 3,
-       PSP_OPT_FACTOR_SLAB_WARPS = 4 };
+       PSP_OPT_FACTOR_SLAB_WARPS = 4, PSP_OPT_FACTOR_PAIRS = 5 };
 psp_status psp_set_option(psp_handle h, int32_t option, int64_t value);
 
 /* Rebind the handle to another stream of the same device. */

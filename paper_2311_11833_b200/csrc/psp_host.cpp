@@ -51,6 +51,7 @@ struct psp_ctx {
   DevicePlan plan;
   psp::LaunchInfo launch;
   int64_t opt_groups = 0, opt_warps = 0, opt_lanes = 0, opt_slab_warps = 0;  // PSP_OPT_FACTOR_*
+  int64_t opt_pairs = 1;                                                      // PSP_OPT_FACTOR_PAIRS
   DevBuf fscratch_d, sscratch_d;   // global pending buffers when shared memory is too small
   DevBuf fscr_d;                   // global l/u scratch rows (large pivots) when needed
 
@@ -225,6 +226,10 @@ psp_status psp_set_option(psp_handle h, int32_t option, int64_t value) {
         return fail(h, PSP_ERR_ARG, "PSP_OPT_FACTOR_LANES must be 0, 1 or 2");
       h->opt_lanes = value;
       return PSP_OK;
+    case PSP_OPT_FACTOR_PAIRS:
+      if (value != 0 && value != 1) return fail(h, PSP_ERR_ARG, "PSP_OPT_FACTOR_PAIRS must be 0 or 1");
+      h->opt_pairs = value;
+      return PSP_OK;
     case PSP_OPT_FACTOR_SLAB_WARPS:
       if (value != 0 && value != 1 && value != 2)
         return fail(h, PSP_ERR_ARG, "PSP_OPT_FACTOR_SLAB_WARPS must be 0, 1 or 2");
@@ -350,6 +355,7 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
   if (nnzLU64 > INT32_MAX / 2) return fail(h, PSP_ERR_ARG, "pattern too large");
 
   psp::HostPlan HP;
+  HP.fuse_pairs = h->opt_pairs != 0;
   psp::build_programs(n, S.lcol, perm, row_ptr_h, col_idx_h, HP);
 
   // CSC grouping of A's entries (original numbering) for the deterministic 1-norm

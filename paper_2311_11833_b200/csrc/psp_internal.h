@@ -22,6 +22,7 @@ constexpr int kDataStages = 2;        // depth of the solve's per-warp factor-ro
 constexpr int kSolveMaxC = 16;        // records with c <= kSolveMaxC take the unrolled path
 constexpr int kMaxWarpsCta = 16;      // consumer warps per CTA (plus one producer warp)
 constexpr int kFusedMax = 16;         // pivots with c <= kFusedMax: u in registers, no scratch
+constexpr int kPairMax = 8;          // supernode pairs for c <= kPairMax
 
 // Record types of the programs (bits 28..31 of a record's first word).
 enum : uint32_t { kRecBirth = 1u, kRecPivot = 2u, kRecUpdate = 3u, kRecEnd = 4u, kRecYEnd = 5u };

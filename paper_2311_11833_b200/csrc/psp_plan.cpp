@@ -290,7 +290,9 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
   //          + c L operands, c U operands (4 words each)
   //          + (flags & 2 == 0) c rows x ws target slots of the c x c update block
   //          flags: 1 = the pivot was never updated (add eps*d_p); 2 = c > kFusedMax,
-  //          the update comes in UPDATE records; ws = row stride (8 * ceil(c / 8))
+  //          the update comes in UPDATE records; 4 = supernode pair: the record also
+  //          carries pivot q = p + 1 (row 0 of the block is q's row, column 0 its column);
+  //          ws = row stride (8 * ceil(c / 8))
   //   BIRTH  [1<<28, 0, nbd, nba, 0, 0, 0, 0] + births: those of the next pivot that do
   //          not fit its record
   //   UPDATE [3<<28 | c, a0, na, ws, 0, 0, 0, 0] + na rows x ws target slots (rows
@@ -342,6 +344,23 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
   };
   P.adiag.assign(n, -1);
   for (int32_t i = 0; i < n; ++i) P.adiag[i] = a_index(i, i);
+  // Supernode pairs: pivot p and q = p + 1 with L(:, p) = {q} u L(:, q) (a fundamental
+  // supernode link, q the etree parent of p) share one record: q's update block is the
+  // trailing part of p's, so the kernel applies both updates to it with one load/store
+  // (in the canonical order: p's, then q's).  Entries first touched at q: none.
+  std::vector<char> paired(n, 0);
+  P.f_pairs = 0;
+  if (P.fuse_pairs)
+    for (int32_t p = 0; p + 1 < n; ++p) {
+      const auto& Lp = lcol[p];
+      const auto& Lq = lcol[p + 1];
+      if (Lp.empty() || Lp[0] != p + 1 || (int32_t)Lp.size() > kPairMax) continue;
+      if (Lp.size() != Lq.size() + 1 || !std::equal(Lq.begin(), Lq.end(), Lp.begin() + 1)) continue;
+      if (!births_at[p + 1].empty()) continue;
+      paired[p] = 1;
+      ++P.f_pairs;
+      ++p;   // q is not the first of another pair
+    }
   for (int32_t p = 0; p < n; ++p) {
     const auto& L = lcol[p];
     const int32_t c = (int32_t)L.size();
@@ -364,7 +383,7 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
       push(std::move(b), std::move(pt));
     }
     const int32_t e_pp = entry(p, p);
-    const int32_t flags = (first[e_pp] < 0 ? 1 : 0) | (fused ? 0 : 2);
+    const int32_t flags = (first[e_pp] < 0 ? 1 : 0) | (fused ? 0 : 2) | (paired[p] ? 4 : 0);
     std::vector<int32_t> r = {(int32_t)((kRecPivot << 28) | (uint32_t)c), p,
                               (int32_t)(bd.size() - qd), (int32_t)(bo.size() - qo), flags, ws};
     std::vector<std::pair<int32_t, int32_t>> pt;
@@ -380,6 +399,7 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
     if (fused)
       for (int32_t a = 0; a < c; ++a) row(r, a);
     push(std::move(r), std::move(pt));
+    if (paired[p]) ++p;   // q's work is in p's record
     if (!fused) {
       const int32_t rows_per = std::max<int32_t>(1, (int32_t)((kMaxRec - 8) / ws));
       for (int32_t a0 = 0; a0 < c; a0 += rows_per) {

@@ -22,7 +22,8 @@ struct HostPlan {
   std::vector<int32_t> adiag;       // [n] CSR index of A's diagonal (permuted numbering) or -1
   // factor program and solve program (forward records, YEND, backward records, END):
   // record streams packed in chunks
-  int32_t f_slots = 0, f_births = 0, f_chunk_words = 0;
+  int32_t f_slots = 0, f_births = 0, f_chunk_words = 0, f_pairs = 0;
+  bool fuse_pairs = true;          // input: fuse supernode pivot pairs into one record
   std::vector<int32_t> f_stream;
   // immediates of the factor stream: word position of each 64-bit cell and its source
   // (>= 0: A index, nnz_A = structural zero; < 0: d[-1 - src], permuted numbering)

@@ -25,7 +25,8 @@ EXPORTS = ["psp_create", "psp_destroy", "psp_set_stream", "psp_status_string",
            "psp_set_perturbations", "psp_factor_batch", "psp_solve_batch", "psp_get_solutions",
            "psp_set_weights", "psp_recover", "psp_get_lane_status", "psp_solve_host",
            "psp_synchronize", "psp_ladder_weights", "psp_set_option", "psp_get_factor"]
-OPT = {"factor_groups": 1, "factor_warps": 2, "factor_lanes": 3, "factor_slab_warps": 4}
+OPT = {"factor_groups": 1, "factor_warps": 2, "factor_lanes": 3, "factor_slab_warps": 4,
+       "factor_pairs": 5}
 
 
 class SymbolicInfo(ctypes.Structure):

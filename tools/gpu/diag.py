@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--grid", type=int, default=300)
     ap.add_argument("--groups", default="0,1:1,2:2,2:1,4:2", help="G:J pairs")
     ap.add_argument("--warps", type=int, default=0)
+    ap.add_argument("--pairs", type=int, default=1)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--R", type=int, default=1)
     a = ap.parse_args()
@@ -41,6 +42,7 @@ def main():
         v, J, P = (int(x) for x in (gj + ":0:0").split(":")[:3])
         sv = psp.Solver(0)
         sv.psp_set_option("factor_groups", v)
+        sv.psp_set_option("factor_pairs", a.pairs)
         sv.psp_set_option("factor_lanes", J)
         sv.psp_set_option("factor_slab_warps", P)
         sv.psp_set_option("factor_warps", a.warps)
