@@ -338,7 +338,8 @@ def main():
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": bdom, "launch_ms": tdom},
-            "gpu_launches": 4 * args.steps,
+            # per step: pivot tolerance, program patch, factor, solve, recover
+            "gpu_launches": 5 * args.steps,
             "clocks": clocks,
             "lane_failures": n_failed,
             "symbolic": info,

@@ -249,12 +249,15 @@ def test_diagonal_closed_form_at_full_size():
     assert np.max(np.abs(err - pred)) <= 16 * np.finfo(float).eps * np.max(np.abs(b / a))
 
 
-@pytest.mark.parametrize("gjp", [(1, 1, 1), (1, 1, 2), (2, 1, 1), (2, 2, 1), (4, 1, 1), (4, 2, 1)])
+@pytest.mark.parametrize("gjp", [(1, 1, 1), (1, 1, 2), (2, 1, 1), (2, 2, 1), (4, 1, 1), (4, 2, 1),
+                                 (1, 1, 1, 0)])
 def test_factor_kernel_variants_bitwise(gjp):
     """Every warp/lane organisation of the factor kernel (G groups per warp, J lanes per
     thread, P warps per slab) keeps the canonical order: lanes bitwise equal to the
     oracle (leading-zero regime, growth ~1/eps, several slabs and a ragged tail)."""
-    G, J, P = gjp
+    G, J, P = gjp[:3]
+    pairs = gjp[3] if len(gjp) > 3 else 1
+    gjp = gjp[:3]
     s = config(1).system()
     rng = np.random.default_rng(7)
     K = 100
@@ -263,6 +266,7 @@ def test_factor_kernel_variants_bitwise(gjp):
     solver.psp_set_option("factor_groups", G)
     solver.psp_set_option("factor_lanes", J)
     solver.psp_set_option("factor_slab_warps", P)
+    solver.psp_set_option("factor_pairs", pairs)
     solver.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering="mindeg_first", first_node=s.slot_p)
     info, perm = solver.psp_get_symbolic_info()
     assert (info["factor_groups"], info["factor_lanes_per_thread"], info["factor_slab_warps"]) == gjp
@@ -275,6 +279,7 @@ def test_factor_kernel_variants_bitwise(gjp):
     # the factor itself, entry by entry, against a G=J=P=1 run
     ref = psp.Solver(0)
     ref.psp_set_option("factor_groups", 1)
+    ref.psp_set_option("factor_pairs", 1 - pairs if gjp == (1, 1, 1) else 1)
     ref.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering="mindeg_first", first_node=s.slot_p)
     ref.psp_set_perturbations(eps, s.d)
     ref.psp_factor_batch(torch.tensor(s.vals, dtype=torch.float64, device="cuda"), 1e-300)
