@@ -261,6 +261,7 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
   }
   std::vector<int32_t> fslot;
   P.f_slots = colour(n, first, death, false, fslot);
+  const int32_t dummy_slot = P.f_slots++;   // target of the padding births (never read)
   P.f_births = 0;
   // inverse entry -> (i, j) for births
   std::vector<int32_t> ent_i(n_ent), ent_j(n_ent);
@@ -286,7 +287,8 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
   //   PIVOT  [2<<28 | c, p, nbd, nba, flags, ws, d_p (2 words)]
   //          + pivot operand (4 words)
   //          + nbd diagonal births  [slot, 0, a_ii (2), d_i (2), 0, 0]: a_ii + eps*d_i
-  //          + nba births           [slot, 0, a_ij (2)] (structural zeros: a_ij = 0)
+  //          + nba births           [slot, 0, a_ij (2)] (structural zeros: a_ij = 0);
+  //            nba is a multiple of 4 (padding births write a dummy slot never read)
   //          + c L operands, c U operands (4 words each)
   //          + (flags & 2 == 0) c rows x ws target slots of the c x c update block
   //          flags: 1 = the pivot was never updated (add eps*d_p); 2 = c > kFusedMax,
@@ -368,7 +370,7 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
     const bool fused = c <= kFusedMax;
     std::vector<int32_t> bd, bo;   // diagonal / other births (entry ids)
     for (int32_t e : births_at[p]) (ent_i[e] == ent_j[e] ? bd : bo).push_back(e);
-    const size_t fixed = 8 + 4 + 8 * (size_t)c + (fused ? (size_t)c * ws : 0);
+    const size_t fixed = 8 + 4 + 12 + 8 * (size_t)c + (fused ? (size_t)c * ws : 0);
     // births that do not fit the pivot's record go first, in BIRTH records
     size_t qd = 0, qo = 0;
     while (fixed + 8 * (bd.size() - qd) + 4 * (bo.size() - qo) > kMaxRec &&
@@ -377,20 +379,23 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
       std::vector<std::pair<int32_t, int32_t>> pt;
       int32_t nd = 0, no = 0;
       while (qd < bd.size() && b.size() + 8 <= kMaxRec) birth(b, pt, bd[qd++]), ++nd;
-      while (qo < bo.size() && b.size() + 4 <= kMaxRec) birth(b, pt, bo[qo++]), ++no;
+      while (qo < bo.size() && b.size() + 4 <= kMaxRec - 12) birth(b, pt, bo[qo++]), ++no;
+      while (no % 4) b.insert(b.end(), {dummy_slot, 0, 0, 0}), ++no;
       b[2] = nd;
       b[3] = no;
       push(std::move(b), std::move(pt));
     }
     const int32_t e_pp = entry(p, p);
     const int32_t flags = (first[e_pp] < 0 ? 1 : 0) | (fused ? 0 : 2) | (paired[p] ? 4 : 0);
+    const int32_t nbo = (int32_t)(bo.size() - qo), nbo4 = (nbo + 3) & ~3;
     std::vector<int32_t> r = {(int32_t)((kRecPivot << 28) | (uint32_t)c), p,
-                              (int32_t)(bd.size() - qd), (int32_t)(bo.size() - qo), flags, ws};
+                              (int32_t)(bd.size() - qd), nbo4, flags, ws};
     std::vector<std::pair<int32_t, int32_t>> pt;
     imm(r, pt, -1 - p);
     operand(r, pt, p, p);
     while (qd < bd.size()) birth(r, pt, bd[qd++]);
     while (qo < bo.size()) birth(r, pt, bo[qo++]);
+    for (int32_t k = nbo; k < nbo4; ++k) r.insert(r.end(), {dummy_slot, 0, 0, 0});
     for (int32_t k = 0; k < c; ++k) operand(r, pt, L[k], p);
     for (int32_t k = 0; k < c; ++k) operand(r, pt, p, L[k]);
     auto row = [&](std::vector<int32_t>& out, int32_t a) {
