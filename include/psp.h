@@ -88,7 +88,9 @@ typedef struct {
                                     32/G*J lanes                                     */
   int32_t factor_slab_warps;     /* P: warps sharing one slab (rows split)          */
   int32_t factor_warps_per_cta;  /* consumer warps per factor CTA                    */
-  int32_t factor_pend_smem;      /* 1: pending slots in shared memory, 0: global     */
+  int32_t factor_pend_smem;      /* 1: pending slots in shared memory, 0: global,
+                                    2: 4 warps per CTA in tensor memory, the rest in
+                                    shared memory (PSP_OPT_FACTOR_TMEM)               */
   int32_t solve_live_smem;       /* 1: solve's live slots in shared memory, 0: global */
 } psp_symbolic_info;
 
@@ -116,9 +118,13 @@ psp_status psp_destroy(psp_handle h);
  *                         L(:,p) = {p+1} u L(:,p+1)) into one record; 0: off.
  *  PSP_OPT_FACTOR_WARPS   0 (default): automatic; else consumer warps per factor CTA
  *                         (1..16, capped by shared memory).
+ *  PSP_OPT_FACTOR_TMEM    0 (default): automatic; 1: require, 2: disable the factor
+ *                         variant whose warps 0..3 keep their pending slots in tensor
+ *                         memory (G = J = P = 1, 2 * slots <= 512).
+ *                         Results are bitwise independent of this option.
  * Errors: ARG. */
 enum { PSP_OPT_FACTOR_GROUPS = 1, PSP_OPT_FACTOR_WARPS = 2, PSP_OPT_FACTOR_LANES = 3,
-       PSP_OPT_FACTOR_SLAB_WARPS = 4, PSP_OPT_FACTOR_PAIRS = 5 };
+       PSP_OPT_FACTOR_SLAB_WARPS = 4, PSP_OPT_FACTOR_PAIRS = 5, PSP_OPT_FACTOR_TMEM = 6 };
 psp_status psp_set_option(psp_handle h, int32_t option, int64_t value);
 
 /* Rebind the handle to another stream of the same device. */

@@ -61,6 +61,8 @@ struct LaunchInfo {
   int f_smem = 0;              // dynamic shared memory per CTA
   int f_off_warp = 0, f_warp_bytes = 0, f_off_scr = 0;
   int f_ctas_per_sm = 0;
+  bool f_tmem = false;         // (1, 1, 1) with warps 0..3 holding their slots in TMEM
+  int f_off_tscr = 0;          // TMEM warps' scratch rows (shared memory)
   // solve
   bool s_live_smem = false;
   bool s_b_smem = true;        // b staged in shared memory (else read from global)
@@ -74,10 +76,12 @@ struct LaunchInfo {
 // force_groups: 0 = automatic, else G in {1, 2, 4, 8}; force_warps: 0 = automatic.
 // Returns false when no configuration fits the shared memory (the program's records or
 // the solve's working set are too large).
+// force_tmem: 0 = automatic, 1 = require the TMEM variant, 2 = disable it.
 bool choose_launch(const DevicePlan& p, LaunchInfo& li, int force_groups, int force_warps,
-                   int force_lanes, int force_slab_warps);
+                   int force_lanes, int force_slab_warps, int force_tmem);
 cudaError_t configure_kernels(const DevicePlan& p, LaunchInfo& li, int force_groups,
-                              int force_warps, int force_lanes, int force_slab_warps);
+                              int force_warps, int force_lanes, int force_slab_warps,
+                              int force_tmem);
 // Fill the factor stream's immediates (A values, d) in `stream_out` (device copy).
 cudaError_t launch_patch_program(const DevicePlan& p, int32_t* stream_out, const double* A_vals,
                                  const double* dperm, cudaStream_t stream);

@@ -287,6 +287,35 @@ def test_factor_kernel_variants_bitwise(gjp):
         assert np.array_equal(solver.psp_get_factor(k, info["nnz_LU"]), ref.psp_get_factor(k, info["nnz_LU"]))
 
 
+@pytest.mark.parametrize("K", [33, 300, 1000])
+def test_factor_tmem_variant_bitwise(K):
+    """The factor variant whose warps 0..3 keep their pending slots in tensor memory
+    (PSP_OPT_FACTOR_TMEM) against the oracle and, factor entry by entry, against the
+    shared-memory variant; K = 33 / 300 / 1000 leave partial last CTAs (TMEM warps only,
+    or some shared-memory warps inactive) and a ragged last slab."""
+    s = config(1).system()
+    rng = np.random.default_rng(K)
+    eps = rng.choice([-1, 1], K) * 10.0 ** rng.uniform(-6, -2, K)
+    out = {}
+    for tm in (1, 2):
+        solver = psp.Solver(0)
+        solver.psp_set_option("factor_tmem", tm)
+        solver.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering="mindeg")
+        info, perm = solver.psp_get_symbolic_info()
+        assert info["factor_pend_smem"] == (2 if tm == 1 else 1)
+        solver.psp_set_perturbations(eps, s.d)
+        solver.psp_factor_batch(torch.tensor(s.vals, dtype=torch.float64, device="cuda"), 1e-300)
+        solver.psp_solve_batch(torch.tensor(s.b.T.copy(), dtype=torch.float64, device="cuda"))
+        out[tm] = (solver, info, perm, solver.psp_get_solutions().cpu().numpy())
+    solver, info, perm, X = out[1]
+    Xo, sto = oracle.SparseOracle(s, perm).batch(eps, 1e-300)
+    assert np.array_equal(X, Xo)
+    assert np.array_equal(X, out[2][3])
+    for k in sorted({0, 31, 32, 127, 128, K // 2, K - 1}):
+        assert np.array_equal(solver.psp_get_factor(k, info["nnz_LU"]),
+                              out[2][0].psp_get_factor(k, info["nnz_LU"]))
+
+
 def test_sharded_recover_partials_sum_to_full():
     """Row a6 on one GPU: lanes split over two handles (a ladder straddles the split);
     each recovers its partial sums with its shard of the weights; their sum equals the

@@ -23,7 +23,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ladders", type=int, default=8192)
     ap.add_argument("--grid", type=int, default=300)
-    ap.add_argument("--groups", default="0,1:1,2:2,2:1,4:2", help="G:J pairs")
+    ap.add_argument("--groups", default="0,1:1,2:2,2:1,4:2", help="G:J[:P[:T]] (T: 0 auto, 1 TMEM, 2 no TMEM)")
     ap.add_argument("--warps", type=int, default=0)
     ap.add_argument("--pairs", type=int, default=1)
     ap.add_argument("--reps", type=int, default=5)
@@ -39,13 +39,14 @@ def main():
     B = torch.tensor(s.b.T.copy(), dtype=torch.float64, device="cuda")
     ref = None
     for gj in a.groups.split(","):
-        v, J, P = (int(x) for x in (gj + ":0:0").split(":")[:3])
+        v, J, P, T = (int(x) for x in (gj + ":0:0:0").split(":")[:4])
         sv = psp.Solver(0)
         sv.psp_set_option("factor_groups", v)
         sv.psp_set_option("factor_pairs", a.pairs)
         sv.psp_set_option("factor_lanes", J)
         sv.psp_set_option("factor_slab_warps", P)
         sv.psp_set_option("factor_warps", a.warps)
+        sv.psp_set_option("factor_tmem", T)
         t0 = time.perf_counter()
         sv.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, "mindeg")
         t_an = time.perf_counter() - t0
