@@ -311,7 +311,7 @@ def test_factor_tmem_variant_bitwise(K):
     Xo, sto = oracle.SparseOracle(s, perm).batch(eps, 1e-300)
     assert np.array_equal(X, Xo)
     assert np.array_equal(X, out[2][3])
-    for k in sorted({0, 31, 32, 127, 128, K // 2, K - 1}):
+    for k in sorted(k for k in {0, 31, 32, 127, 128, K // 2, K - 1} if k < K):
         assert np.array_equal(solver.psp_get_factor(k, info["nnz_LU"]),
                               out[2][0].psp_get_factor(k, info["nnz_LU"]))
 
