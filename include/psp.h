@@ -91,7 +91,8 @@ typedef struct {
   int32_t factor_pend_smem;      /* 1: pending slots in shared memory, 0: global,
                                     2: 4 warps per CTA in tensor memory, the rest in
                                     shared memory (PSP_OPT_FACTOR_TMEM)               */
-  int32_t solve_live_smem;       /* 1: solve's live slots in shared memory, 0: global */
+  int32_t solve_live_smem;       /* 1: solve's live slots in shared memory, 0: global,
+                                    2: tensor memory (PSP_OPT_SOLVE_TMEM)             */
 } psp_symbolic_info;
 
 /* ---- lifetime ---------------------------------------------------------------- */
@@ -122,9 +123,13 @@ psp_status psp_destroy(psp_handle h);
  *                         variant whose warps 0..3 keep their pending slots in tensor
  *                         memory (G = J = P = 1, 2 * slots <= 512).
  *                         Results are bitwise independent of this option.
+ *  PSP_OPT_SOLVE_TMEM     0 (default) or 2: off; 1: require the solve
+ *                         variant that keeps its live y/x slots in tensor memory
+ *                         (DESIGN.md §5).  Results are bitwise independent of it.
  * Errors: ARG. */
 enum { PSP_OPT_FACTOR_GROUPS = 1, PSP_OPT_FACTOR_WARPS = 2, PSP_OPT_FACTOR_LANES = 3,
-       PSP_OPT_FACTOR_SLAB_WARPS = 4, PSP_OPT_FACTOR_PAIRS = 5, PSP_OPT_FACTOR_TMEM = 6 };
+       PSP_OPT_FACTOR_SLAB_WARPS = 4, PSP_OPT_FACTOR_PAIRS = 5, PSP_OPT_FACTOR_TMEM = 6,
+       PSP_OPT_SOLVE_TMEM = 7 };
 psp_status psp_set_option(psp_handle h, int32_t option, int64_t value);
 
 /* Rebind the handle to another stream of the same device. */

@@ -53,6 +53,7 @@ struct psp_ctx {
   int64_t opt_groups = 0, opt_warps = 0, opt_lanes = 0, opt_slab_warps = 0;  // PSP_OPT_FACTOR_*
   int64_t opt_pairs = 1;                                                      // PSP_OPT_FACTOR_PAIRS
   int64_t opt_tmem = 0;                                                       // PSP_OPT_FACTOR_TMEM
+  int64_t opt_solve_tmem = 0;                                                 // PSP_OPT_SOLVE_TMEM
   DevBuf fscratch_d, sscratch_d;   // global pending buffers when shared memory is too small
   DevBuf fscr_d;                   // global l/u scratch rows (large pivots) when needed
 
@@ -230,6 +231,10 @@ psp_status psp_set_option(psp_handle h, int32_t option, int64_t value) {
     case PSP_OPT_FACTOR_TMEM:
       if (value < 0 || value > 2) return fail(h, PSP_ERR_ARG, "PSP_OPT_FACTOR_TMEM must be 0, 1 or 2");
       h->opt_tmem = value;
+      return PSP_OK;
+    case PSP_OPT_SOLVE_TMEM:
+      if (value < 0 || value > 2) return fail(h, PSP_ERR_ARG, "PSP_OPT_SOLVE_TMEM must be 0, 1 or 2");
+      h->opt_solve_tmem = value;
       return PSP_OK;
     case PSP_OPT_FACTOR_PAIRS:
       if (value != 0 && value != 1) return fail(h, PSP_ERR_ARG, "PSP_OPT_FACTOR_PAIRS must be 0 or 1");
@@ -412,13 +417,15 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
   UP(acsc_q, acsc_q);
 #undef UP
   if (!psp::choose_launch(P, h->launch, (int)h->opt_groups, (int)h->opt_warps,
-                          (int)h->opt_lanes, (int)h->opt_slab_warps, (int)h->opt_tmem))
+                          (int)h->opt_lanes, (int)h->opt_slab_warps, (int)h->opt_tmem,
+                          (int)h->opt_solve_tmem))
     return fail(h, PSP_ERR_UNSUPPORTED, "no kernel configuration fits shared memory "
                 "(program chunk %d words, c_max %d, solve live slots %d)", P.f_chunk_words,
                 P.c_max, P.y_slots + P.x_slots);
   if (!host_only)
     CUDA_TRY(h, psp::configure_kernels(P, h->launch, (int)h->opt_groups, (int)h->opt_warps,
-                                        (int)h->opt_lanes, (int)h->opt_slab_warps, (int)h->opt_tmem));
+                                        (int)h->opt_lanes, (int)h->opt_slab_warps, (int)h->opt_tmem,
+                          (int)h->opt_solve_tmem));
   h->plan = P;
   h->perm = perm;
   h->n = n;
@@ -456,7 +463,7 @@ psp_status psp_get_symbolic_info(psp_handle h, psp_symbolic_info* info, int32_t*
   info->factor_slab_warps = h->launch.f_slab_warps;
   info->factor_warps_per_cta = h->launch.f_warps;
   info->factor_pend_smem = h->launch.f_tmem ? 2 : (h->launch.f_pend_smem ? 1 : 0);
-  info->solve_live_smem = h->launch.s_live_smem ? 1 : 0;
+  info->solve_live_smem = h->launch.s_tmem ? 2 : (h->launch.s_live_smem ? 1 : 0);
   info->solve_live = h->y_slots + h->x_slots;
   info->births = h->f_births;
   if (perm_h) std::copy(h->perm.begin(), h->perm.end(), perm_h);
@@ -545,7 +552,7 @@ psp_status psp_solve_batch(psp_handle h, int32_t R, const double* B, int64_t ldb
     if ((s = ensure(h, h->X_d, need))) return s;
   }
   if (!h->launch.s_live_smem) {
-    size_t need2 = sizeof(double) * (size_t)h->K_pad * (h->plan.y_slots + h->plan.x_slots);
+    size_t need2 = sizeof(double) * (size_t)h->K_pad * (h->plan.y_slots + h->plan.x_slots + 1);
     if (h->sscratch_d.bytes < need2) {
       CUDA_TRY(h, cudaStreamSynchronize(h->stream));
       if ((s = ensure(h, h->sscratch_d, need2))) return s;

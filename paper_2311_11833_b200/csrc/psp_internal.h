@@ -70,18 +70,21 @@ struct LaunchInfo {
   int s_smem = 0;
   int s_off_b = 0, s_off_warp = 0, s_warp_bytes = 0, s_off_data = 0;
   int s_ctas_per_sm = 0;
+  bool s_tmem = false;         // live slots in tensor memory (solve_kernel_tmem)
+  int s_tmem_cols = 0;         // TMEM columns allocated per CTA
 };
 
 // Kernel launchers (psp_kernels.cu).  All asynchronous on `stream`.
 // force_groups: 0 = automatic, else G in {1, 2, 4, 8}; force_warps: 0 = automatic.
 // Returns false when no configuration fits the shared memory (the program's records or
 // the solve's working set are too large).
-// force_tmem: 0 = automatic, 1 = require the TMEM variant, 2 = disable it.
+// force_tmem / force_solve_tmem: 0 = automatic, 1 = require the factor's / solve's TMEM
+// variant, 2 = disable it.
 bool choose_launch(const DevicePlan& p, LaunchInfo& li, int force_groups, int force_warps,
-                   int force_lanes, int force_slab_warps, int force_tmem);
+                   int force_lanes, int force_slab_warps, int force_tmem, int force_solve_tmem);
 cudaError_t configure_kernels(const DevicePlan& p, LaunchInfo& li, int force_groups,
                               int force_warps, int force_lanes, int force_slab_warps,
-                              int force_tmem);
+                              int force_tmem, int force_solve_tmem);
 // Fill the factor stream's immediates (A values, d) in `stream_out` (device copy).
 cudaError_t launch_patch_program(const DevicePlan& p, int32_t* stream_out, const double* A_vals,
                                  const double* dperm, cudaStream_t stream);

@@ -290,8 +290,9 @@ def test_factor_kernel_variants_bitwise(gjp):
 @pytest.mark.parametrize("K", [33, 300, 1000])
 def test_factor_tmem_variant_bitwise(K):
     """The factor variant whose warps 0..3 keep their pending slots in tensor memory
-    (PSP_OPT_FACTOR_TMEM) against the oracle and, factor entry by entry, against the
-    shared-memory variant; K = 33 / 300 / 1000 leave partial last CTAs (TMEM warps only,
+    (PSP_OPT_FACTOR_TMEM) and the solve variant with its live slots in tensor memory
+    (PSP_OPT_SOLVE_TMEM) against the oracle and, factor entry by entry, against the
+    shared-memory variants; K = 33 / 300 / 1000 leave partial last CTAs (TMEM warps only,
     or some shared-memory warps inactive) and a ragged last slab."""
     s = config(1).system()
     rng = np.random.default_rng(K)
@@ -300,9 +301,11 @@ def test_factor_tmem_variant_bitwise(K):
     for tm in (1, 2):
         solver = psp.Solver(0)
         solver.psp_set_option("factor_tmem", tm)
+        solver.psp_set_option("solve_tmem", tm)
         solver.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering="mindeg")
         info, perm = solver.psp_get_symbolic_info()
         assert info["factor_pend_smem"] == (2 if tm == 1 else 1)
+        assert info["solve_live_smem"] == (2 if tm == 1 else 1)
         solver.psp_set_perturbations(eps, s.d)
         solver.psp_factor_batch(torch.tensor(s.vals, dtype=torch.float64, device="cuda"), 1e-300)
         solver.psp_solve_batch(torch.tensor(s.b.T.copy(), dtype=torch.float64, device="cuda"))

@@ -39,7 +39,7 @@ def main():
     B = torch.tensor(s.b.T.copy(), dtype=torch.float64, device="cuda")
     ref = None
     for gj in a.groups.split(","):
-        v, J, P, T = (int(x) for x in (gj + ":0:0:0").split(":")[:4])
+        v, J, P, T, S = (int(x) for x in (gj + ":0:0:0:0").split(":")[:5])
         sv = psp.Solver(0)
         sv.psp_set_option("factor_groups", v)
         sv.psp_set_option("factor_pairs", a.pairs)
@@ -47,6 +47,7 @@ def main():
         sv.psp_set_option("factor_slab_warps", P)
         sv.psp_set_option("factor_warps", a.warps)
         sv.psp_set_option("factor_tmem", T)
+        sv.psp_set_option("solve_tmem", S)
         t0 = time.perf_counter()
         sv.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, "mindeg")
         t_an = time.perf_counter() - t0
