@@ -3,8 +3,10 @@
 
 One STEP = one pass of the whole hot path (SURVEY §8(a) rows a1-a5, a6 when the
 recovered sums are split across ranks) over one batch: perturb + pivot-free LU of K
-lanes (psp_factor_batch), forward/back substitution (psp_solve_batch) and the
-weighted recombination (psp_recover).  Symbolic analysis (row a0) is done once per
+lanes with the forward substitution fused in (psp_factor_solve_batch: the factor
+kernel eliminates [A | b]), the backward substitution, and the weighted
+recombination (psp_recover).  `--separate` times psp_factor_batch + psp_solve_batch
+instead (bitwise the same results).  Symbolic analysis (row a0) is done once per
 pattern, outside the timed region, and reported separately.
 
 Workload (N=1 line): the BASELINE configs[1] system — the synthetic 300-bus
@@ -192,6 +194,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--groups", type=int, default=0, help="PSP_OPT_FACTOR_GROUPS (0 = auto)")
     ap.add_argument("--warps", type=int, default=0, help="PSP_OPT_FACTOR_WARPS (0 = auto)")
+    ap.add_argument("--separate", action="store_true",
+                    help="factor_batch + solve_batch instead of the fused factor_solve_batch")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -217,6 +221,7 @@ def main():
     solver = psp.Solver(local_rank, stream)
     solver.psp_set_option("factor_groups", args.groups)
     solver.psp_set_option("factor_warps", args.warps)
+    solver.psp_set_option("phase_events", 1)
     t0 = time.perf_counter()
     solver.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering="mindeg")
     t_sym = time.perf_counter() - t0
@@ -232,15 +237,16 @@ def main():
     def step(ev=None):
         if ev is not None:
             ev[0].record(stream)
-        solver.psp_factor_batch(A, 0.0)
+        if args.separate:
+            solver.psp_factor_batch(A, 0.0)
+            solver.psp_solve_batch(B)
+        else:
+            solver.psp_factor_solve_batch(A, B, 0.0)
         if ev is not None:
             ev[1].record(stream)
-        solver.psp_solve_batch(B)
-        if ev is not None:
-            ev[2].record(stream)
         solver.psp_recover(xh)
         if ev is not None:
-            ev[3].record(stream)
+            ev[2].record(stream)
 
     clk = ClockSampler(local_rank) if rank == 0 else None
     for _ in range(args.warmup):
@@ -249,7 +255,8 @@ def main():
     rc, st = solver.psp_get_lane_status()
     n_failed = int((st != 0).sum())
 
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    solver.psp_get_phase_times()   # (drops the warm-up launches' events)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -268,9 +275,11 @@ def main():
         dist.barrier()
     clocks = clk.stop() if clk else None
     ms_total = start.elapsed_time(end)
-    t_factor = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
-    t_solve = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
-    t_recover = sum(e[2].elapsed_time(e[3]) for e in evs) / args.steps
+    # factor / solve kernel times: the library's events around its launches in the
+    # timed region (PSP_OPT_PHASE_EVENTS), averaged over the K steps
+    t_factor, t_solve = solver.psp_get_phase_times()
+    t_call = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
+    t_recover = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
     if world > 1:
         tt = torch.tensor([ms_total], device="cuda", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -300,8 +309,13 @@ def main():
         nnzLU, n, R = info["nnz_LU"], s.n, 1
         # algorithmic bytes per launch: the factor kernel's output is the
         # 8*nnz_LU values of every lane (A and eps/d reads are shared and negligible)
-        bytes_factor = 8.0 * nnzLU * K + 8.0 * s.nnz + 16.0 * K
-        bytes_solve = 8.0 * nnzLU * K + 8.0 * n * R * K + 8.0 * n * R
+        nnzDU = nnzLU - info["nnz_L"]
+        if args.separate:
+            bytes_factor = 8.0 * nnzLU * K + 8.0 * s.nnz + 16.0 * K
+            bytes_solve = 8.0 * nnzLU * K + 8.0 * n * R * K + 8.0 * n * R
+        else:   # fused: the factor also writes y (n per lane); the solve reads DU + y, writes x
+            bytes_factor = 8.0 * nnzLU * K + 8.0 * n * K + 8.0 * s.nnz + 8.0 * n + 16.0 * K
+            bytes_solve = 8.0 * nnzDU * K + 16.0 * n * K
         bytes_recover = 8.0 * n * R * K + 8.0 * W * R * n
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
             if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
@@ -332,7 +346,9 @@ def main():
                        "l2": "no flush: 2.9 GB factor written per step > 126 MB L2"},
             "recovered_solves_per_s": rec_value,
             "phases_ms": {"factor": t_factor, "solve": t_solve, "recover": t_recover,
-                          "symbolic_once": 1e3 * t_sym},
+                          "factor_solve_call": t_call, "symbolic_once": 1e3 * t_sym},
+            "path": "factor_batch + solve_batch" if args.separate else
+                    "factor_solve_batch (forward fused into the factor)",
             "hbm_gbs_algorithmic": (bytes_factor + bytes_solve + bytes_recover) / (ms_step * 1e-3) / 1e9,
             "roofline": {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,

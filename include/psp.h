@@ -12,6 +12,7 @@
  *   psp_set_perturbations  signed eps_k per lane and d          (Alg. 1 step 1)
  *   psp_factor_batch       batched pivot-free numeric LU         (Alg. 1 step 2)
  *   psp_solve_batch        batched forward/back substitution     (Alg. 1 step 2)
+ *   psp_factor_solve_batch the two fused for one right-hand side (Alg. 1 step 2)
  *   psp_set_weights +
  *   psp_recover            x_hat[w] = sum_k w[w][k] x_k          (Alg. 1 steps 3-4,
  *                                                                 Eq. (13)/(14))
@@ -93,6 +94,8 @@ typedef struct {
                                     shared memory (PSP_OPT_FACTOR_TMEM)               */
   int32_t solve_live_smem;       /* 1: solve's live slots in shared memory, 0: global,
                                     2: tensor memory (PSP_OPT_SOLVE_TMEM)             */
+  /* the augmented program of psp_factor_solve_batch ([A | b]; aug_ok = 0: unavailable) */
+  int32_t aug_ok, aug_max_live, aug_warps_per_cta, aug_pend_smem;
 } psp_symbolic_info;
 
 /* ---- lifetime ---------------------------------------------------------------- */
@@ -126,10 +129,12 @@ psp_status psp_destroy(psp_handle h);
  *  PSP_OPT_SOLVE_TMEM     0 (default) or 2: off; 1: require the solve
  *                         variant that keeps its live y/x slots in tensor memory
  *                         (DESIGN.md §5).  Results are bitwise independent of it.
- * Errors: ARG. */
+ *  PSP_OPT_PHASE_EVENTS   0 (default); 1: record CUDA events around the factor and the
+ *                         solve kernel launches (for psp_get_phase_times; any time).
+ * Errors: ARG (STATE: PSP_OPT_PHASE_EVENTS on a host-only handle). */
 enum { PSP_OPT_FACTOR_GROUPS = 1, PSP_OPT_FACTOR_WARPS = 2, PSP_OPT_FACTOR_LANES = 3,
        PSP_OPT_FACTOR_SLAB_WARPS = 4, PSP_OPT_FACTOR_PAIRS = 5, PSP_OPT_FACTOR_TMEM = 6,
-       PSP_OPT_SOLVE_TMEM = 7 };
+       PSP_OPT_SOLVE_TMEM = 7, PSP_OPT_PHASE_EVENTS = 8 };
 psp_status psp_set_option(psp_handle h, int32_t option, int64_t value);
 
 /* Rebind the handle to another stream of the same device. */
@@ -186,6 +191,24 @@ psp_status psp_factor_batch(psp_handle h, const double* A_vals, double pivot_tol
  * the ORIGINAL ordering.  Solutions stay in library memory (see psp_get_solutions).
  * Errors: ARG, STATE, ALLOC, CUDA. */
 psp_status psp_solve_batch(psp_handle h, int32_t R, const double* B, int64_t ldb);
+
+/* psp_factor_batch + psp_solve_batch for ONE right-hand side b (device, n values,
+ * ORIGINAL ordering) with the forward substitution fused into the factorisation:
+ * the factor kernel eliminates the augmented matrix [A | b] (b as a column that is
+ * never a pivot), so y = L^{-1} b is produced by the same updates, in the same
+ * canonical order (y_i = fma(-l_ip, y_p, y_i), p ascending), as the separate forward
+ * pass would, and the solve runs the backward pass only.  Results (factor, lane
+ * statuses, solutions) are bitwise those of psp_factor_batch + psp_solve_batch with
+ * R = 1.  Saves the forward pass's read of L and its interpretation overhead
+ * (DESIGN.md §5).  Errors: ARG, STATE, UNSUPPORTED (the augmented program fits no
+ * factor configuration), ALLOC, CUDA. */
+psp_status psp_factor_solve_batch(psp_handle h, const double* A_vals, const double* b,
+                                  double pivot_tol, int32_t* lane_status);
+
+/* With PSP_OPT_PHASE_EVENTS on: device time (ms, cudaEventElapsedTime) of the last
+ * factor kernel (ms_h[0]) and the last solve kernel (ms_h[1]) launched by the calls
+ * above; synchronises on the last solve.  Errors: ARG, STATE, CUDA. */
+psp_status psp_get_phase_times(psp_handle h, float* ms_h);
 
 /* Copy the per-lane solutions to X (device, K x R x n, lane-major, ORIGINAL
  * ordering): X[(k*R + r)*n + i] = x_k,r[i].  Errors: ARG, STATE. */

@@ -50,12 +50,22 @@ struct psp_ctx {
   std::vector<DevBuf> plan_bufs;
   DevicePlan plan;
   psp::LaunchInfo launch;
+  // program of the augmented matrix [A | b] (psp_factor_solve_batch); its own slots,
+  // stream and factor launch configuration, the rest shared with `plan`
+  DevicePlan plan_aug;
+  psp::LaunchInfo launch_aug;
+  bool aug_ok = false;
   int64_t opt_groups = 0, opt_warps = 0, opt_lanes = 0, opt_slab_warps = 0;  // PSP_OPT_FACTOR_*
   int64_t opt_pairs = 1;                                                      // PSP_OPT_FACTOR_PAIRS
   int64_t opt_tmem = 0;                                                       // PSP_OPT_FACTOR_TMEM
   int64_t opt_solve_tmem = 0;                                                 // PSP_OPT_SOLVE_TMEM
   DevBuf fscratch_d, sscratch_d;   // global pending buffers when shared memory is too small
   DevBuf fscr_d;                   // global l/u scratch rows (large pivots) when needed
+  // PSP_OPT_PHASE_EVENTS: event pairs around every factor / solve kernel launch since
+  // the last psp_get_phase_times (pools grow on demand, reused after a read)
+  bool phase_events = false;
+  std::vector<cudaEvent_t> fev, sev;
+  size_t nf = 0, ns = 0;
 
   // --- perturbations ---
   int32_t K = 0, K_pad = 0;
@@ -211,6 +221,8 @@ psp_status psp_destroy(psp_handle h) {
   h->stageA_d.release();
   h->stageB_d.release();
   h->stageX_d.release();
+  for (auto* v : {&h->fev, &h->sev})
+    for (cudaEvent_t e : *v) cudaEventDestroy(e);
   delete h;
   return PSP_OK;
 }
@@ -231,6 +243,12 @@ psp_status psp_set_option(psp_handle h, int32_t option, int64_t value) {
     case PSP_OPT_FACTOR_TMEM:
       if (value < 0 || value > 2) return fail(h, PSP_ERR_ARG, "PSP_OPT_FACTOR_TMEM must be 0, 1 or 2");
       h->opt_tmem = value;
+      return PSP_OK;
+    case PSP_OPT_PHASE_EVENTS:
+      if (value != 0 && value != 1) return fail(h, PSP_ERR_ARG, "PSP_OPT_PHASE_EVENTS must be 0 or 1");
+      if (value && h->device < 0) return fail(h, PSP_ERR_STATE, "host-only handle");
+      h->phase_events = value != 0;
+      h->nf = h->ns = 0;
       return PSP_OK;
     case PSP_OPT_SOLVE_TMEM:
       if (value < 0 || value > 2) return fail(h, PSP_ERR_ARG, "PSP_OPT_SOLVE_TMEM must be 0, 1 or 2");
@@ -364,9 +382,11 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
   for (int32_t j = 0; j < n; ++j) nnzLU64 += 2 * (int64_t)S.lcol[j].size();
   if (nnzLU64 > INT32_MAX / 2) return fail(h, PSP_ERR_ARG, "pattern too large");
 
-  psp::HostPlan HP;
-  HP.fuse_pairs = h->opt_pairs != 0;
+  psp::HostPlan HP, HPa;
+  HP.fuse_pairs = HPa.fuse_pairs = h->opt_pairs != 0;
+  HPa.aug = true;
   psp::build_programs(n, S.lcol, perm, row_ptr_h, col_idx_h, HP);
+  psp::build_programs(n, S.lcol, perm, row_ptr_h, col_idx_h, HPa);
 
   // CSC grouping of A's entries (original numbering) for the deterministic 1-norm
   std::vector<int32_t> acsc_ptr(n + 1, 0), acsc_q(nnzA);
@@ -396,6 +416,7 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
   P.s_rows = HP.s_rows;
   P.s_nfwd = HP.s_nfwd;
   P.s_nfc = (int32_t)HP.s_fchunks.size() / 2;
+  P.s_bwd_chunk = HP.s_bwd_chunk;
   psp_status s;
 #define UP(vec, field) \
   if (!host_only && (s = upload(h, vec, &P.field))) return s;
@@ -426,6 +447,25 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
     CUDA_TRY(h, psp::configure_kernels(P, h->launch, (int)h->opt_groups, (int)h->opt_warps,
                                         (int)h->opt_lanes, (int)h->opt_slab_warps, (int)h->opt_tmem,
                           (int)h->opt_solve_tmem));
+  // the augmented program: same layout and solve; its own factor stream, slots, launch
+  DevicePlan Pa = P;
+  Pa.f_aug = 1;
+  Pa.f_slots = HPa.f_slots;
+  Pa.f_chunk_words = HPa.f_chunk_words;
+  Pa.f_nchunks = (int32_t)(HPa.f_stream.size() / HPa.f_chunk_words);
+  Pa.c_scr = HP.c_max + 1 > psp::kFusedMax ? HP.c_max + 1 : 0;
+  Pa.f_npatch = (int32_t)HPa.f_patch_pos.size();
+  psp::LaunchInfo la = h->launch;
+  // (the augmented factor kernels exist for G = J = P = 1 only)
+  h->aug_ok = (h->opt_groups <= 1 && h->opt_lanes <= 1 && h->opt_slab_warps <= 1) &&
+              psp::choose_launch(Pa, la, 1, (int)h->opt_warps, 1, 1, (int)h->opt_tmem, 2);
+  if (h->aug_ok && !host_only) {   // (its stream is patched in place, like plan's)
+    if ((s = upload(h, HPa.f_stream, &Pa.f_stream))) return s;
+    if ((s = upload(h, HPa.f_patch_pos, &Pa.f_patch_pos))) return s;
+    if ((s = upload(h, HPa.f_patch_src, &Pa.f_patch_src))) return s;
+  }
+  h->plan_aug = Pa;
+  h->launch_aug = la;
   h->plan = P;
   h->perm = perm;
   h->n = n;
@@ -465,6 +505,10 @@ psp_status psp_get_symbolic_info(psp_handle h, psp_symbolic_info* info, int32_t*
   info->factor_pend_smem = h->launch.f_tmem ? 2 : (h->launch.f_pend_smem ? 1 : 0);
   info->solve_live_smem = h->launch.s_tmem ? 2 : (h->launch.s_live_smem ? 1 : 0);
   info->solve_live = h->y_slots + h->x_slots;
+  info->aug_ok = h->aug_ok ? 1 : 0;
+  info->aug_max_live = h->plan_aug.f_slots;
+  info->aug_warps_per_cta = h->aug_ok ? h->launch_aug.f_warps : 0;
+  info->aug_pend_smem = !h->aug_ok ? 0 : (h->launch_aug.f_tmem ? 2 : (h->launch_aug.f_pend_smem ? 1 : 0));
   info->births = h->f_births;
   if (perm_h) std::copy(h->perm.begin(), h->perm.end(), perm_h);
   return PSP_OK;
@@ -498,45 +542,112 @@ psp_status psp_set_perturbations(psp_handle h, int32_t K, const double* eps_h, c
   return PSP_OK;
 }
 
-psp_status psp_factor_batch(psp_handle h, const double* A_vals, double pivot_tol,
-                            int32_t* lane_status) {
+// Record the next event of a phase pool on the handle's stream (growing the pool).
+static psp_status phase_mark(psp_ctx* h, std::vector<cudaEvent_t>& pool, size_t& used) {
+  if (used == pool.size()) {
+    cudaEvent_t e;
+    CUDA_TRY(h, cudaEventCreate(&e));
+    pool.push_back(e);
+  }
+  CUDA_TRY(h, cudaEventRecord(pool[used++], h->stream));
+  return PSP_OK;
+}
+
+// Factorisation of the K perturbed copies with `plan` (aug = false) or of the augmented
+// [A | b] with `plan_aug` (aug = true: y = L^{-1} b goes to X).
+static psp_status factor_impl(psp_handle h, const double* A_vals, double pivot_tol,
+                              int32_t* lane_status, bool aug, const double* b) {
   if (!h) return PSP_ERR_ARG;
   if (!h->analysed || h->K == 0) return fail(h, PSP_ERR_STATE, "set_perturbations first");
   if (!A_vals) return fail(h, PSP_ERR_ARG, "A_vals required");
   if (!(pivot_tol == pivot_tol)) return fail(h, PSP_ERR_ARG, "pivot_tol is NaN");
+  const DevicePlan& P = aug ? h->plan_aug : h->plan;
+  const psp::LaunchInfo& LI = aug ? h->launch_aug : h->launch;
   cudaSetDevice(h->device);
+  psp_status s;
   const double* tol_dev = nullptr;
   if (pivot_tol <= 0) {
-    CUDA_TRY(h, psp::launch_pivot_tol(h->plan, A_vals, (double*)h->tol_d.p, h->stream));
+    CUDA_TRY(h, psp::launch_pivot_tol(P, A_vals, (double*)h->tol_d.p, h->stream));
     tol_dev = (const double*)h->tol_d.p;
   }
-  if (!h->launch.f_pend_smem) {
-    psp_status s;
-    size_t need = sizeof(double) * (size_t)h->K_pad * h->plan.f_slots;
+  if (!LI.f_pend_smem) {
+    size_t need = sizeof(double) * (size_t)h->K_pad * P.f_slots;
     if (h->fscratch_d.bytes < need) {
       CUDA_TRY(h, cudaStreamSynchronize(h->stream));
       if ((s = ensure(h, h->fscratch_d, need))) return s;
     }
   }
-  CUDA_TRY(h, psp::launch_patch_program(h->plan, const_cast<int32_t*>(h->plan.f_stream), A_vals,
-                                        (const double*)h->dperm_d.p, h->stream));
-  if (!h->launch.f_scr_smem) {
-    psp_status s;
-    size_t need = sizeof(double) * (size_t)h->K_pad * 2 * h->plan.c_scr;
+  if (aug) {
+    size_t need = sizeof(double) * (size_t)h->K_pad * h->n;
+    if (h->X_d.bytes < need) {
+      CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+      if ((s = ensure(h, h->X_d, need))) return s;
+    }
+  }
+  CUDA_TRY(h, psp::launch_patch_program(P, const_cast<int32_t*>(P.f_stream), A_vals,
+                                        (const double*)h->dperm_d.p, b, h->stream));
+  if (!LI.f_scr_smem) {
+    size_t need = sizeof(double) * (size_t)h->K_pad * 2 * P.c_scr;
     if (h->fscr_d.bytes < need) {
       CUDA_TRY(h, cudaStreamSynchronize(h->stream));
       if ((s = ensure(h, h->fscr_d, need))) return s;
     }
   }
-  CUDA_TRY(h, psp::launch_factor(h->plan, h->launch, h->plan.f_stream, (const double*)h->eps_d.p,
-                                 tol_dev, pivot_tol, (double*)h->V_d.p, (double*)h->fscratch_d.p,
-                                 (double*)h->fscr_d.p, (int32_t*)h->status_d.p, h->K_pad,
-                                 h->stream));
+  if (h->phase_events) {
+    if ((s = phase_mark(h, h->fev, h->nf))) return s;
+  }
+  CUDA_TRY(h, psp::launch_factor(P, LI, P.f_stream, (const double*)h->eps_d.p, tol_dev, pivot_tol,
+                                 (double*)h->V_d.p, (double*)h->fscratch_d.p, (double*)h->fscr_d.p,
+                                 (int32_t*)h->status_d.p, h->K_pad,
+                                 aug ? (double*)h->X_d.p : nullptr, h->stream));
+  if (h->phase_events) {
+    if ((s = phase_mark(h, h->fev, h->nf))) return s;
+  }
   if (lane_status)
     CUDA_TRY(h, cudaMemcpyAsync(lane_status, h->status_d.p, sizeof(int32_t) * h->K,
                                 cudaMemcpyDeviceToDevice, h->stream));
   h->factored = true;
   h->solved = h->recovered = false;
+  return PSP_OK;
+}
+
+psp_status psp_factor_batch(psp_handle h, const double* A_vals, double pivot_tol,
+                            int32_t* lane_status) {
+  return factor_impl(h, A_vals, pivot_tol, lane_status, false, nullptr);
+}
+
+static psp_status solve_scratch(psp_handle h) {
+  psp_status s;
+  if (!h->launch.s_live_smem) {
+    size_t need2 = sizeof(double) * (size_t)h->K_pad * (h->plan.y_slots + h->plan.x_slots + 1);
+    if (h->sscratch_d.bytes < need2) {
+      CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+      if ((s = ensure(h, h->sscratch_d, need2))) return s;
+    }
+  }
+  return PSP_OK;
+}
+
+psp_status psp_factor_solve_batch(psp_handle h, const double* A_vals, const double* b,
+                                  double pivot_tol, int32_t* lane_status) {
+  if (!h) return PSP_ERR_ARG;
+  if (!b) return fail(h, PSP_ERR_ARG, "b required");
+  if (h->analysed && !h->aug_ok)
+    return fail(h, PSP_ERR_UNSUPPORTED, "no factor configuration fits the augmented program");
+  psp_status s = factor_impl(h, A_vals, pivot_tol, lane_status, true, b);
+  if (s) return s;
+  if ((s = solve_scratch(h))) return s;
+  if (h->phase_events) {
+    if ((s = phase_mark(h, h->sev, h->ns))) return s;
+  }
+  CUDA_TRY(h, psp::launch_solve(h->plan, h->launch, (const double*)h->V_d.p, b, h->n, 1,
+                                (double*)h->X_d.p, (double*)h->sscratch_d.p, h->K_pad, false,
+                                h->stream));
+  if (h->phase_events) {
+    if ((s = phase_mark(h, h->sev, h->ns))) return s;
+  }
+  h->R = 1;
+  h->solved = true;
   return PSP_OK;
 }
 
@@ -551,18 +662,38 @@ psp_status psp_solve_batch(psp_handle h, int32_t R, const double* B, int64_t ldb
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     if ((s = ensure(h, h->X_d, need))) return s;
   }
-  if (!h->launch.s_live_smem) {
-    size_t need2 = sizeof(double) * (size_t)h->K_pad * (h->plan.y_slots + h->plan.x_slots + 1);
-    if (h->sscratch_d.bytes < need2) {
-      CUDA_TRY(h, cudaStreamSynchronize(h->stream));
-      if ((s = ensure(h, h->sscratch_d, need2))) return s;
-    }
+  if ((s = solve_scratch(h))) return s;
+  if (h->phase_events) {
+    if ((s = phase_mark(h, h->sev, h->ns))) return s;
   }
   CUDA_TRY(h, psp::launch_solve(h->plan, h->launch, (const double*)h->V_d.p, B, ldb, R,
-                                (double*)h->X_d.p, (double*)h->sscratch_d.p, h->K_pad,
+                                (double*)h->X_d.p, (double*)h->sscratch_d.p, h->K_pad, true,
                                 h->stream));
+  if (h->phase_events) {
+    if ((s = phase_mark(h, h->sev, h->ns))) return s;
+  }
   h->R = R;
   h->solved = true;
+  return PSP_OK;
+}
+
+psp_status psp_get_phase_times(psp_handle h, float* ms_h) {
+  if (!h || !ms_h) return PSP_ERR_ARG;
+  if (!h->phase_events) return fail(h, PSP_ERR_STATE, "PSP_OPT_PHASE_EVENTS is off");
+  cudaSetDevice(h->device);
+  for (int q = 0; q < 2; ++q) {
+    const std::vector<cudaEvent_t>& v = q ? h->sev : h->fev;
+    const size_t m = q ? h->ns : h->nf;
+    double sum = 0.0;
+    for (size_t k = 0; k + 1 < m; k += 2) {
+      float t = 0.f;
+      CUDA_TRY(h, cudaEventSynchronize(v[k + 1]));
+      CUDA_TRY(h, cudaEventElapsedTime(&t, v[k], v[k + 1]));
+      sum += t;
+    }
+    ms_h[q] = m >= 2 ? (float)(sum / (double)(m / 2)) : 0.f;
+  }
+  h->nf = h->ns = 0;
   return PSP_OK;
 }
 
@@ -684,8 +815,14 @@ psp_status psp_solve_host(psp_handle h, const double* A_vals_h, int32_t R, const
                               cudaMemcpyHostToDevice, h->stream));
   CUDA_TRY(h, cudaMemcpyAsync(h->stageB_d.p, B_h, sizeof(double) * (size_t)h->n * R,
                               cudaMemcpyHostToDevice, h->stream));
-  if ((s = psp_factor_batch(h, (const double*)h->stageA_d.p, pivot_tol, nullptr))) return s;
-  if ((s = psp_solve_batch(h, R, (const double*)h->stageB_d.p, h->n))) return s;
+  if (R == 1 && h->aug_ok) {   // one right-hand side: forward pass fused into the factor
+    if ((s = psp_factor_solve_batch(h, (const double*)h->stageA_d.p, (const double*)h->stageB_d.p,
+                                    pivot_tol, nullptr)))
+      return s;
+  } else {
+    if ((s = psp_factor_batch(h, (const double*)h->stageA_d.p, pivot_tol, nullptr))) return s;
+    if ((s = psp_solve_batch(h, R, (const double*)h->stageB_d.p, h->n))) return s;
+  }
   if ((s = psp_recover(h, (double*)h->stageX_d.p))) return s;
   CUDA_TRY(h, cudaMemcpyAsync(x_h, h->stageX_d.p, sizeof(double) * (size_t)h->W * R * h->n,
                               cudaMemcpyDeviceToHost, h->stream));

@@ -39,11 +39,13 @@ struct DevicePlan {
   int32_t f_npatch = 0;
   const int32_t* f_patch_pos = nullptr;
   const int32_t* f_patch_src = nullptr;
+  int32_t f_aug = 0;                   // 1: program of [A | b] (y_p written to X)
   // solve program: forward (ascending) records, YEND, backward (descending) records, END
   int32_t y_slots = 0, x_slots = 0, s_chunk_words = 0, s_nchunks = 0;
   const int32_t* s_stream = nullptr;
   int32_t s_rows = 16, s_nfwd = 0, s_nfc = 0;   // ring stage rows; forward / all row chunks
   const int2* s_fchunks = nullptr;              // [s_nfc] row ranges [r0, r1)
+  int32_t s_bwd_chunk = 0;                      // first chunk of the backward records
   // deterministic column sums for the default pivot tolerance
   const int32_t* acsc_ptr = nullptr;   // [n+1]
   const int32_t* acsc_q = nullptr;     // [nnz_A]
@@ -85,18 +87,19 @@ bool choose_launch(const DevicePlan& p, LaunchInfo& li, int force_groups, int fo
 cudaError_t configure_kernels(const DevicePlan& p, LaunchInfo& li, int force_groups,
                               int force_warps, int force_lanes, int force_slab_warps,
                               int force_tmem, int force_solve_tmem);
-// Fill the factor stream's immediates (A values, d) in `stream_out` (device copy).
+// Fill the factor stream's immediates (A values, d, b for the augmented program) in
+// `stream_out` (device copy).
 cudaError_t launch_patch_program(const DevicePlan& p, int32_t* stream_out, const double* A_vals,
-                                 const double* dperm, cudaStream_t stream);
+                                 const double* dperm, const double* b, cudaStream_t stream);
 cudaError_t launch_pivot_tol(const DevicePlan& p, const double* A_vals, double* tol_out,
                              cudaStream_t stream);
 cudaError_t launch_factor(const DevicePlan& p, const LaunchInfo& li, const int32_t* prog,
                           const double* eps, const double* tol_dev, double tol_value, double* V,
                           double* gscratch, double* gscr, int32_t* status, int32_t K_pad,
-                          cudaStream_t stream);
+                          double* Y, cudaStream_t stream);
 cudaError_t launch_solve(const DevicePlan& p, const LaunchInfo& li, const double* V,
                          const double* B, int64_t ldb, int32_t R, double* X, double* gscratch,
-                         int32_t K_pad, cudaStream_t stream);
+                         int32_t K_pad, bool forward, cudaStream_t stream);
 cudaError_t launch_recover(const DevicePlan& p, int32_t W, int32_t R, const int32_t* w_ptr,
                            const int32_t* w_lane, const double* w_val, const double* X,
                            const int32_t* status, double* x_out, int32_t* infeasible_flag,

@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdint>
 #include <functional>
 #include <cstdlib>
 #include <set>
@@ -177,18 +178,20 @@ void pack_chunks(const std::vector<std::vector<int32_t>>& recs, size_t max_rec,
                  int32_t& chunk_words, std::vector<int32_t>& out,
                  const std::vector<std::vector<std::pair<int32_t, int32_t>>>* patches = nullptr,
                  std::vector<int32_t>* patch_pos = nullptr,
-                 std::vector<int32_t>* patch_src = nullptr) {
+                 std::vector<int32_t>* patch_src = nullptr, size_t break_at = SIZE_MAX,
+                 int32_t* break_chunk = nullptr) {
   chunk_words = 512;  // 2 KB
   while ((size_t)chunk_words < max_rec + 4) chunk_words *= 2;
   out.assign(chunk_words, -1);
   size_t base = 0, used = 0;
   for (size_t k = 0; k < recs.size(); ++k) {
     const auto& r = recs[k];
-    if (used + r.size() + 4 > (size_t)chunk_words) {
+    if (used + r.size() + 4 > (size_t)chunk_words || (k == break_at && used > 0)) {
       base += chunk_words;
       used = 0;
       out.resize(base + chunk_words, -1);
     }
+    if (k == break_at && break_chunk) *break_chunk = (int32_t)(base / chunk_words);
     std::copy(r.begin(), r.end(), out.begin() + base + used);
     if (patches)
       for (const auto& pr : (*patches)[k]) {
@@ -235,7 +238,10 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
   // entry ids: diag p -> p; L(i,j) (i>j) -> n + off[j] + pos; U(i,j) (i<j) -> n + nnzL + off[i] + pos
   std::vector<int32_t> off(n + 1, 0);
   for (int32_t p = 0; p < n; ++p) off[p + 1] = off[p] + (int32_t)lcol[p].size();
-  const int32_t n_ent = n + 2 * (int32_t)nnzL;
+  // augmented: entry n + 2 nnzL + i = (i, b), the right-hand side column
+  const bool aug = P.aug;
+  const int32_t n_ent = n + 2 * (int32_t)nnzL + (aug ? n : 0);
+  auto entry_b = [&](int32_t i) -> int32_t { return n + 2 * (int32_t)nnzL + i; };
   auto pos_in = [&](int32_t col, int32_t row) -> int32_t {
     const auto& v = lcol[col];
     return (int32_t)(std::lower_bound(v.begin(), v.end(), row) - v.begin());
@@ -258,6 +264,14 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
           death[e] = std::min(a, b);
         }
       }
+    if (aug)
+      for (int32_t a : L) {
+        const int32_t e = entry_b(a);
+        if (first[e] < 0) {
+          first[e] = p;
+          death[e] = a;
+        }
+      }
   }
   std::vector<int32_t> fslot;
   P.f_slots = colour(n, first, death, false, fslot);
@@ -273,6 +287,10 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
       ent_j[n + off[p] + k] = p;
       ent_i[n + nnzL + off[p] + k] = p;  // U(p, i)
       ent_j[n + nnzL + off[p] + k] = i;
+    }
+    if (aug) {
+      ent_i[entry_b(p)] = p;  // (p, b): j = n marks the right-hand side
+      ent_j[entry_b(p)] = n;
     }
   }
   std::vector<std::vector<int32_t>> births_at(n);
@@ -322,22 +340,26 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
     r.push_back(0);
     r.push_back(0);
   };
+  // A value (or b_i for j = n) of entry (i, j) as an immediate source
+  auto a_src = [&](int32_t i, int32_t j) -> int32_t {
+    if (j == n) return nnzA + 1 + perm[i];
+    const int32_t q = a_index(i, j);
+    return q >= 0 ? q : nnzA;
+  };
   auto operand = [&](std::vector<int32_t>& r, std::vector<std::pair<int32_t, int32_t>>& pt,
                      int32_t i, int32_t j) {
-    const int32_t e = entry(i, j);
+    const int32_t e = j == n ? entry_b(i) : entry(i, j);
     if (first[e] >= 0) {
       r.insert(r.end(), {fslot[e], 0, 0, 0});
     } else {
-      const int32_t q = a_index(i, j);
       r.insert(r.end(), {-1, 0});
-      imm(r, pt, q >= 0 ? q : nnzA);
+      imm(r, pt, a_src(i, j));
     }
   };
   auto birth = [&](std::vector<int32_t>& r, std::vector<std::pair<int32_t, int32_t>>& pt, int32_t e) {
     const int32_t i = ent_i[e], j = ent_j[e];
-    const int32_t q = a_index(i, j);
     r.insert(r.end(), {fslot[e], 0});
-    imm(r, pt, q >= 0 ? q : nnzA);
+    imm(r, pt, a_src(i, j));
     if (i == j) {
       imm(r, pt, -1 - i);
       r.insert(r.end(), {0, 0});
@@ -356,7 +378,7 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
     for (int32_t p = 0; p + 1 < n; ++p) {
       const auto& Lp = lcol[p];
       const auto& Lq = lcol[p + 1];
-      if (Lp.empty() || Lp[0] != p + 1 || (int32_t)Lp.size() > kPairMax) continue;
+      if (Lp.empty() || Lp[0] != p + 1 || (int32_t)Lp.size() + (aug ? 1 : 0) > kPairMax) continue;
       if (Lp.size() != Lq.size() + 1 || !std::equal(Lq.begin(), Lq.end(), Lp.begin() + 1)) continue;
       if (!births_at[p + 1].empty()) continue;
       paired[p] = 1;
@@ -366,11 +388,12 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
   for (int32_t p = 0; p < n; ++p) {
     const auto& L = lcol[p];
     const int32_t c = (int32_t)L.size();
-    const int32_t ws = 8 * ((c + 7) / 8);
-    const bool fused = c <= kFusedMax;
+    const int32_t cu = c + (aug ? 1 : 0);   // U-row columns (+ the right-hand side)
+    const int32_t ws = 8 * ((cu + 7) / 8);
+    const bool fused = cu <= kFusedMax;
     std::vector<int32_t> bd, bo;   // diagonal / other births (entry ids)
     for (int32_t e : births_at[p]) (ent_i[e] == ent_j[e] ? bd : bo).push_back(e);
-    const size_t fixed = 8 + 4 + 12 + 8 * (size_t)c + (fused ? (size_t)c * ws : 0);
+    const size_t fixed = 8 + 4 + 12 + 4 * (size_t)(c + cu) + (fused ? (size_t)c * ws : 0);
     // births that do not fit the pivot's record go first, in BIRTH records
     size_t qd = 0, qo = 0;
     while (fixed + 8 * (bd.size() - qd) + 4 * (bo.size() - qo) > kMaxRec &&
@@ -398,8 +421,10 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
     for (int32_t k = nbo; k < nbo4; ++k) r.insert(r.end(), {dummy_slot, 0, 0, 0});
     for (int32_t k = 0; k < c; ++k) operand(r, pt, L[k], p);
     for (int32_t k = 0; k < c; ++k) operand(r, pt, p, L[k]);
+    if (aug) operand(r, pt, p, n);   // y_p
     auto row = [&](std::vector<int32_t>& out, int32_t a) {
-      for (int32_t b = 0; b < ws; ++b) out.push_back(b < c ? fslot[entry(L[a], L[b])] : 0);
+      for (int32_t b = 0; b < ws; ++b)
+        out.push_back(b < c ? fslot[entry(L[a], L[b])] : (b < cu ? fslot[entry_b(L[a])] : 0));
     };
     if (fused)
       for (int32_t a = 0; a < c; ++a) row(r, a);
@@ -468,6 +493,7 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
     }
     spush({(int32_t)(kRecYEnd << 28), 0, 0, 0});
   }
+  const size_t bwd_first = srec.size();   // the backward records start a chunk
   {
     // step s = n-1-i; x_i born at the step of i, dies at the step of the smallest q with
     // i in lcol(q)
@@ -487,7 +513,8 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
     }
     spush({(int32_t)(kRecEnd << 28), 0, 0, 0});
   }
-  pack_chunks(srec, smax, P.s_chunk_words, P.s_stream);
+  pack_chunks(srec, smax, P.s_chunk_words, P.s_stream, nullptr, nullptr, nullptr, bwd_first,
+              &P.s_bwd_chunk);
 
   // Factor-row chunks of the solve, in consumption order: the L region ascending
   // (forward), then the DU region descending (backward).  A chunk holds <= s_rows rows

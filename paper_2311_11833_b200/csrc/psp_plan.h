@@ -24,9 +24,14 @@ struct HostPlan {
   // record streams packed in chunks
   int32_t f_slots = 0, f_births = 0, f_chunk_words = 0, f_pairs = 0;
   bool fuse_pairs = true;          // input: fuse supernode pivot pairs into one record
+  // input: factor program of the AUGMENTED matrix [A | b] (column n = one right-hand
+  // side, never a pivot): every U row gets u_{p b} = y_p, the forward-substitution
+  // result, which the factor kernel writes to X instead of the DU region
+  bool aug = false;
   std::vector<int32_t> f_stream;
   // immediates of the factor stream: word position of each 64-bit cell and its source
-  // (>= 0: A index, nnz_A = structural zero; < 0: d[-1 - src], permuted numbering)
+  // (>= 0: A index, nnz_A = structural zero, nnz_A + 1 + i: b[i] (original numbering);
+  // < 0: d[-1 - src], permuted numbering)
   std::vector<int32_t> f_patch_pos, f_patch_src;
   int32_t y_slots = 0, x_slots = 0, s_chunk_words = 0;
   std::vector<int32_t> s_stream;
@@ -34,6 +39,7 @@ struct HostPlan {
   // are the forward pass's), at most s_rows rows each
   int32_t s_rows = 16, s_nfwd = 0;
   std::vector<int32_t> s_fchunks;
+  int32_t s_bwd_chunk = 0;         // first program chunk of the backward records
 };
 
 std::vector<int32_t> min_degree_order(int32_t n, const std::vector<std::vector<int32_t>>& adj,

@@ -22,11 +22,12 @@ ORDER = {"natural": 0, "mindeg": 1, "user": 2, "mindeg_first": 3}
 
 EXPORTS = ["psp_create", "psp_destroy", "psp_set_stream", "psp_status_string",
            "psp_last_error_detail", "psp_symbolic_analyse", "psp_get_symbolic_info",
-           "psp_set_perturbations", "psp_factor_batch", "psp_solve_batch", "psp_get_solutions",
+           "psp_set_perturbations", "psp_factor_batch", "psp_solve_batch", "psp_factor_solve_batch",
+           "psp_get_solutions", "psp_get_phase_times",
            "psp_set_weights", "psp_recover", "psp_get_lane_status", "psp_solve_host",
            "psp_synchronize", "psp_ladder_weights", "psp_set_option", "psp_get_factor"]
 OPT = {"factor_groups": 1, "factor_warps": 2, "factor_lanes": 3, "factor_slab_warps": 4,
-       "factor_pairs": 5, "factor_tmem": 6, "solve_tmem": 7}
+       "factor_pairs": 5, "factor_tmem": 6, "solve_tmem": 7, "phase_events": 8}
 
 
 class SymbolicInfo(ctypes.Structure):
@@ -38,7 +39,9 @@ class SymbolicInfo(ctypes.Structure):
                 ("births", ctypes.c_int32), ("factor_groups", ctypes.c_int32),
                 ("factor_lanes_per_thread", ctypes.c_int32), ("factor_slab_warps", ctypes.c_int32),
                 ("factor_warps_per_cta", ctypes.c_int32), ("factor_pend_smem", ctypes.c_int32),
-                ("solve_live_smem", ctypes.c_int32)]
+                ("solve_live_smem", ctypes.c_int32), ("aug_ok", ctypes.c_int32),
+                ("aug_max_live", ctypes.c_int32), ("aug_warps_per_cta", ctypes.c_int32),
+                ("aug_pend_smem", ctypes.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -71,6 +74,8 @@ def lib():
             "psp_set_perturbations": [P, I32, P, P],
             "psp_factor_batch": [P, P, D, P],
             "psp_solve_batch": [P, I32, P, I64],
+            "psp_factor_solve_batch": [P, P, P, D, P],
+            "psp_get_phase_times": [P, P],
             "psp_get_solutions": [P, P],
             "psp_set_weights": [P, I32, P, P, P],
             "psp_recover": [P, P],
@@ -182,6 +187,25 @@ class Solver:
         assert n == self.n and B.is_contiguous()
         self._check(lib().psp_solve_batch(self.h, R, _t_ptr(B), n))
         self.R = R
+
+    def psp_factor_solve_batch(self, A_vals, b, pivot_tol=0.0, lane_status=None):
+        """Factor + solve for one right-hand side b (device float64 [n] or [1, n]),
+        forward substitution fused into the factorisation (psp.h)."""
+        self._check_dev(A_vals, self.torch.float64, (self.nnz_A,))
+        self._check_dev(b, self.torch.float64, None)
+        assert b.numel() == self.n and b.is_contiguous()
+        ls = None
+        if lane_status is not None:
+            self._check_dev(lane_status, self.torch.int32, (self.K,))
+            ls = _t_ptr(lane_status)
+        self._check(lib().psp_factor_solve_batch(self.h, _t_ptr(A_vals), _t_ptr(b), float(pivot_tol), ls))
+        self.R = 1
+
+    def psp_get_phase_times(self):
+        """(factor_ms, solve_ms) of the last factor / solve kernels (phase_events on)."""
+        ms = (ctypes.c_float * 2)()
+        self._check(lib().psp_get_phase_times(self.h, ms))
+        return float(ms[0]), float(ms[1])
 
     def psp_get_solutions(self, out=None):
         out = out if out is not None else self.torch.empty((self.K, self.R, self.n), dtype=self.torch.float64,

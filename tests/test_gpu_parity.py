@@ -319,6 +319,41 @@ def test_factor_tmem_variant_bitwise(K):
                               out[2][0].psp_get_factor(k, info["nnz_LU"]))
 
 
+@pytest.mark.parametrize("ci,K", [(0, 37), (1, 33), (1, 1000), (2, 300)])
+def test_fused_factor_solve_bitwise(ci, K):
+    """psp_factor_solve_batch (forward substitution fused into the factorisation of
+    [A | b]) against the oracle, and against factor_batch + solve_batch: solutions,
+    lane statuses and the factor itself bitwise equal (ragged K, several CTAs)."""
+    s = config(ci).system()
+    rng = np.random.default_rng(K + 17 * ci)
+    eps = rng.choice([-1, 1], K) * 10.0 ** rng.uniform(-6, -2, K)
+    A = torch.tensor(s.vals, dtype=torch.float64, device="cuda")
+    b = torch.tensor(s.b[:, 0].copy(), dtype=torch.float64, device="cuda")
+    outs = []
+    for fused in (True, False):
+        solver = psp.Solver(0)
+        solver.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering="mindeg")
+        info, perm = solver.psp_get_symbolic_info()
+        solver.psp_set_perturbations(eps, s.d)
+        if fused:
+            solver.psp_factor_solve_batch(A, b, 0.0)
+        else:
+            solver.psp_factor_batch(A, 0.0)
+            solver.psp_solve_batch(b.view(1, -1))
+        X = solver.psp_get_solutions().cpu().numpy()
+        rc, st = solver.psp_get_lane_status()
+        F = [solver.psp_get_factor(k, info["nnz_LU"]) for k in sorted({0, K // 2, K - 1})]
+        outs.append((X, st, F))
+    tol = oracle.default_tol(s.n, s.row_ptr, s.col_idx, s.vals)
+    Xo, sto = oracle.SparseOracle(s, perm).batch(eps, tol, B=s.b[:, :1])
+    X, st, F = outs[0]
+    ok = sto == 0
+    assert np.array_equal(st != 0, sto != 0)
+    assert np.array_equal(X[ok], Xo[ok])
+    assert np.array_equal(X[ok], outs[1][0][ok]) and np.array_equal(st, outs[1][1])
+    assert all(np.array_equal(f1, f2) for f1, f2 in zip(F, outs[1][2]))
+
+
 def test_sharded_recover_partials_sum_to_full():
     """Row a6 on one GPU: lanes split over two handles (a ladder straddles the split);
     each recovers its partial sums with its shard of the weights; their sum equals the
