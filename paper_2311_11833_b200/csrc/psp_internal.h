@@ -21,7 +21,7 @@ constexpr int kYRows = 16;            // y rows per stage of the solve's y ring
 constexpr int kDataStages = 2;        // depth of the solve's per-warp factor-row ring
 constexpr int kSolveMaxC = 16;        // records with c <= kSolveMaxC take the unrolled path
 constexpr int kMaxWarpsCta = 16;      // consumer warps per CTA (plus one producer warp)
-constexpr int kFusedMax = 16;         // pivots with c <= kFusedMax: u in registers, no scratch
+constexpr int kFusedMax = 12;         // pivots with c <= kFusedMax: u in registers, no scratch
 constexpr int kPairMax = 8;          // supernode pairs for c <= kPairMax
 
 // Record types of the programs (bits 28..31 of a record's first word).
