@@ -38,6 +38,7 @@ struct DevBuf {
 
 struct psp_ctx {
   int device = 0;
+  int n_sm = 148;                  // SMs of the device (wave counts of the solve launch)
   cudaStream_t stream = nullptr;
   std::string detail;
 
@@ -50,6 +51,10 @@ struct psp_ctx {
   std::vector<DevBuf> plan_bufs;
   DevicePlan plan;
   psp::LaunchInfo launch;
+  // the solve with its live slots in TMEM (more warps per SM, more instructions per
+  // row): used when it needs fewer waves than `launch`'s (PSP_OPT_SOLVE_TMEM = 0)
+  psp::LaunchInfo launch_stm;
+  bool stm_ok = false;
   // program of the augmented matrix [A | b] (psp_factor_solve_batch); its own slots,
   // stream and factor launch configuration, the rest shared with `plan`
   DevicePlan plan_aug;
@@ -202,6 +207,9 @@ psp_status psp_create(psp_handle* out, int32_t device, void* cuda_stream) {
   if (!h) return PSP_ERR_ALLOC;
   h->device = device;
   h->stream = static_cast<cudaStream_t>(cuda_stream);
+  int nsm = 0;
+  if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && nsm > 0)
+    h->n_sm = nsm;
   *out = h;
   return PSP_OK;
 }
@@ -447,6 +455,15 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
     CUDA_TRY(h, psp::configure_kernels(P, h->launch, (int)h->opt_groups, (int)h->opt_warps,
                                         (int)h->opt_lanes, (int)h->opt_slab_warps, (int)h->opt_tmem,
                           (int)h->opt_solve_tmem));
+  h->stm_ok = false;
+  if (h->opt_solve_tmem == 0) {
+    psp::LaunchInfo ls = h->launch;
+    if (psp::choose_launch(P, ls, (int)h->opt_groups, (int)h->opt_warps, (int)h->opt_lanes,
+                           (int)h->opt_slab_warps, (int)h->opt_tmem, 1)) {
+      h->launch_stm = ls;
+      h->stm_ok = true;
+    }
+  }
   // the augmented program: same layout and solve; its own factor stream, slots, launch
   DevicePlan Pa = P;
   Pa.f_aug = 1;
@@ -542,6 +559,18 @@ psp_status psp_set_perturbations(psp_handle h, int32_t K, const double* eps_h, c
   return PSP_OK;
 }
 
+// The solve's launch configuration for this batch: the TMEM one when it needs fewer
+// waves (rounds of resident warps over the SMs), else the shared-memory one.
+static const psp::LaunchInfo& solve_launch(psp_ctx* h) {
+  if (!h->stm_ok) return h->launch;
+  const int64_t blocks = h->K_pad / psp::kBlock;
+  auto rounds = [&](const psp::LaunchInfo& li) {
+    const int64_t per = (int64_t)li.s_warps * std::max(1, li.s_ctas_per_sm) * h->n_sm;
+    return (blocks + per - 1) / per;
+  };
+  return rounds(h->launch_stm) < rounds(h->launch) ? h->launch_stm : h->launch;
+}
+
 // Record the next event of a phase pool on the handle's stream (growing the pool).
 static psp_status phase_mark(psp_ctx* h, std::vector<cudaEvent_t>& pool, size_t& used) {
   if (used == pool.size()) {
@@ -618,7 +647,7 @@ psp_status psp_factor_batch(psp_handle h, const double* A_vals, double pivot_tol
 
 static psp_status solve_scratch(psp_handle h) {
   psp_status s;
-  if (!h->launch.s_live_smem) {
+  if (!solve_launch(h).s_live_smem) {
     size_t need2 = sizeof(double) * (size_t)h->K_pad * (h->plan.y_slots + h->plan.x_slots + 1);
     if (h->sscratch_d.bytes < need2) {
       CUDA_TRY(h, cudaStreamSynchronize(h->stream));
@@ -640,7 +669,7 @@ psp_status psp_factor_solve_batch(psp_handle h, const double* A_vals, const doub
   if (h->phase_events) {
     if ((s = phase_mark(h, h->sev, h->ns))) return s;
   }
-  CUDA_TRY(h, psp::launch_solve(h->plan, h->launch, (const double*)h->V_d.p, b, h->n, 1,
+  CUDA_TRY(h, psp::launch_solve(h->plan, solve_launch(h), (const double*)h->V_d.p, b, h->n, 1,
                                 (double*)h->X_d.p, (double*)h->sscratch_d.p, h->K_pad, false,
                                 h->stream));
   if (h->phase_events) {
@@ -666,7 +695,7 @@ psp_status psp_solve_batch(psp_handle h, int32_t R, const double* B, int64_t ldb
   if (h->phase_events) {
     if ((s = phase_mark(h, h->sev, h->ns))) return s;
   }
-  CUDA_TRY(h, psp::launch_solve(h->plan, h->launch, (const double*)h->V_d.p, B, ldb, R,
+  CUDA_TRY(h, psp::launch_solve(h->plan, solve_launch(h), (const double*)h->V_d.p, B, ldb, R,
                                 (double*)h->X_d.p, (double*)h->sscratch_d.p, h->K_pad, true,
                                 h->stream));
   if (h->phase_events) {

@@ -73,6 +73,7 @@ struct LaunchInfo {
   int s_off_b = 0, s_off_warp = 0, s_warp_bytes = 0, s_off_data = 0;
   int s_ctas_per_sm = 0;
   bool s_tmem = false;         // live slots in tensor memory (solve_kernel_tmem)
+  int s_yrows = 16;            // rows per stage of the solve's y ring
   int s_tmem_cols = 0;         // TMEM columns allocated per CTA
 };
 
