@@ -18,6 +18,8 @@ for K in [int(k) for k in (sys.argv[1] if len(sys.argv) > 1 else "33,1000,8192,6
     for fused in (False, True):
         sv = psp.Solver(0)
         sv.psp_set_option("solve_tmem", int(os.environ.get("PSP_STM", "0")))
+        sv.psp_set_option("factor_warps", int(os.environ.get("PSP_FW", "0")))
+        sv.psp_set_option("factor_tmem", int(os.environ.get("PSP_FT", "0")))
         sv.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, "mindeg")
         info, perm = sv.psp_get_symbolic_info()
         sv.psp_set_perturbations(eps, s.d)
@@ -42,7 +44,7 @@ for K in [int(k) for k in (sys.argv[1] if len(sys.argv) > 1 else "33,1000,8192,6
         rc, st = sv.psp_get_lane_status()
         out.append((X, F, st))
         print(f"K={K} fused={fused} {min(ts[1:]):.3f} ms (first part {min(t1[1:]):.3f}) rc={rc}"
-              f" solve_live_smem={info['solve_live_smem']}", flush=True)
+              f" solve_live_smem={info['solve_live_smem']} aug warps={info['aug_warps_per_cta']} pend={info['aug_pend_smem']}", flush=True)
         sv.close()
     same = np.array_equal(out[0][0], out[1][0]) and all(np.array_equal(a, c) for a, c in zip(out[0][1], out[1][1])) \
         and np.array_equal(out[0][2], out[1][2])
