@@ -16,7 +16,8 @@ namespace psp {
 constexpr int kBlock = 32;
 // Source codes of the factor program: >= 0 pending slot; otherwise A[-1 - code] of A
 // extended by one structural zero, A[nnz_A] = 0.
-constexpr int kStages = 4;            // depth of the CTA-shared program ring
+constexpr int kStages = 4;            // depth of the CTA-shared program ring (solve)
+constexpr int kFMaxStages = 8;        // factor ring: 4 or 8 stages (LaunchInfo::f_stages)
 constexpr int kYRows = 16;            // y rows per stage of the solve's y ring
 constexpr int kDataStages = 2;        // depth of the solve's per-warp factor-row ring
 constexpr int kSolveMaxC = 16;        // records with c <= kSolveMaxC take the unrolled path
@@ -63,6 +64,7 @@ struct LaunchInfo {
   int f_smem = 0;              // dynamic shared memory per CTA
   int f_off_warp = 0, f_warp_bytes = 0, f_off_scr = 0;
   int f_ctas_per_sm = 0;
+  int f_stages = 4;            // program ring stages of the factor (4 or 8)
   bool f_tmem = false;         // (1, 1, 1) with warps 0..3 holding their slots in TMEM
   int f_off_tscr = 0;          // TMEM warps' scratch rows (shared memory)
   // solve
