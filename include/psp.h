@@ -249,7 +249,17 @@ psp_status psp_get_lane_status(psp_handle h, int32_t* status_h);
 psp_status psp_solve_host(psp_handle h, const double* A_vals_h, int32_t R, const double* B_h,
                           double pivot_tol, double* x_h);
 
-/* Synchronise the handle's stream. */
+/* Pipelined form of psp_solve_host for a stream of systems: enqueues the same work
+ * (copies up, factor + solve + recover, x_h copied back on a second, library-owned
+ * stream from a double-buffered device staging area) and returns without waiting, so
+ * the copy back of one call overlaps the next call's kernels.  A_vals_h, B_h and x_h
+ * must be pinned and stay valid (x_h unread) until psp_synchronize; lane statuses via
+ * psp_get_lane_status afterwards.  Errors: ARG, STATE, ALLOC, CUDA. */
+psp_status psp_solve_host_async(psp_handle h, const double* A_vals_h, int32_t R, const double* B_h,
+                                double pivot_tol, double* x_h);
+
+/* Synchronise the handle's streams (its stream and the copy stream of
+ * psp_solve_host_async). */
 psp_status psp_synchronize(psp_handle h);
 
 /* ---- host helper (pure) --------------------------------------------------------- */

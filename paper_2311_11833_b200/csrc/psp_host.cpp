@@ -91,6 +91,12 @@ struct psp_ctx {
 
   // --- host-API staging ---
   DevBuf stageA_d, stageB_d, stageX_d;
+  // psp_solve_host_async: x-hat staging double buffer, D2H on a copy stream
+  DevBuf stageX2_d;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t x_ready[2] = {nullptr, nullptr}, x_copied[2] = {nullptr, nullptr};
+  bool x_copied_set[2] = {false, false};
+  int pipe = 0;
 };
 
 static psp_status fail(psp_ctx* h, psp_status s, const char* fmt, ...) {
@@ -229,6 +235,15 @@ psp_status psp_destroy(psp_handle h) {
   h->stageA_d.release();
   h->stageB_d.release();
   h->stageX_d.release();
+  h->stageX2_d.release();
+  if (h->copy_stream) {
+    cudaStreamSynchronize(h->copy_stream);
+    cudaStreamDestroy(h->copy_stream);
+  }
+  for (int q = 0; q < 2; ++q) {
+    if (h->x_ready[q]) cudaEventDestroy(h->x_ready[q]);
+    if (h->x_copied[q]) cudaEventDestroy(h->x_copied[q]);
+  }
   for (auto* v : {&h->fev, &h->sev})
     for (cudaEvent_t e : *v) cudaEventDestroy(e);
   delete h;
@@ -291,6 +306,55 @@ psp_status psp_synchronize(psp_handle h) {
   if (!h) return PSP_ERR_ARG;
   if (h->device < 0) return PSP_OK;
   CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  if (h->copy_stream) CUDA_TRY(h, cudaStreamSynchronize(h->copy_stream));
+  return PSP_OK;
+}
+
+psp_status psp_solve_host_async(psp_handle h, const double* A_vals_h, int32_t R, const double* B_h,
+                                double pivot_tol, double* x_h) {
+  if (!h || !A_vals_h || !B_h || !x_h || R < 1) return PSP_ERR_ARG;
+  if (h->K == 0 || h->W == 0) return fail(h, PSP_ERR_STATE, "set_perturbations and set_weights first");
+  cudaSetDevice(h->device);
+  psp_status s;
+  if (!h->copy_stream) {
+    CUDA_TRY(h, cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+    for (int q = 0; q < 2; ++q) {
+      CUDA_TRY(h, cudaEventCreateWithFlags(&h->x_ready[q], cudaEventDisableTiming));
+      CUDA_TRY(h, cudaEventCreateWithFlags(&h->x_copied[q], cudaEventDisableTiming));
+    }
+  }
+  const int q = h->pipe;
+  DevBuf& xs = q ? h->stageX2_d : h->stageX_d;
+  const size_t xbytes = sizeof(double) * (size_t)h->W * R * h->n;
+  if (xs.bytes < xbytes || h->stageA_d.bytes < sizeof(double) * h->nnz_A ||
+      h->stageB_d.bytes < sizeof(double) * (size_t)h->n * R) {
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->copy_stream));
+    if ((s = ensure(h, h->stageA_d, sizeof(double) * h->nnz_A))) return s;
+    if ((s = ensure(h, h->stageB_d, sizeof(double) * (size_t)h->n * R))) return s;
+    if ((s = ensure(h, xs, xbytes))) return s;
+  }
+  // the buffer's previous copy to the host must be done before recover overwrites it
+  if (h->x_copied_set[q]) CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->x_copied[q], 0));
+  CUDA_TRY(h, cudaMemcpyAsync(h->stageA_d.p, A_vals_h, sizeof(double) * h->nnz_A,
+                              cudaMemcpyHostToDevice, h->stream));
+  CUDA_TRY(h, cudaMemcpyAsync(h->stageB_d.p, B_h, sizeof(double) * (size_t)h->n * R,
+                              cudaMemcpyHostToDevice, h->stream));
+  if (R == 1 && h->aug_ok) {
+    if ((s = psp_factor_solve_batch(h, (const double*)h->stageA_d.p, (const double*)h->stageB_d.p,
+                                    pivot_tol, nullptr)))
+      return s;
+  } else {
+    if ((s = psp_factor_batch(h, (const double*)h->stageA_d.p, pivot_tol, nullptr))) return s;
+    if ((s = psp_solve_batch(h, R, (const double*)h->stageB_d.p, h->n))) return s;
+  }
+  if ((s = psp_recover(h, (double*)xs.p))) return s;
+  CUDA_TRY(h, cudaEventRecord(h->x_ready[q], h->stream));
+  CUDA_TRY(h, cudaStreamWaitEvent(h->copy_stream, h->x_ready[q], 0));
+  CUDA_TRY(h, cudaMemcpyAsync(x_h, xs.p, xbytes, cudaMemcpyDeviceToHost, h->copy_stream));
+  CUDA_TRY(h, cudaEventRecord(h->x_copied[q], h->copy_stream));
+  h->x_copied_set[q] = true;
+  h->pipe ^= 1;
   return PSP_OK;
 }
 
@@ -837,6 +901,7 @@ psp_status psp_solve_host(psp_handle h, const double* A_vals_h, int32_t R, const
   if (h->K == 0 || h->W == 0) return fail(h, PSP_ERR_STATE, "set_perturbations and set_weights first");
   cudaSetDevice(h->device);
   psp_status s;
+  if (h->copy_stream) CUDA_TRY(h, cudaStreamSynchronize(h->copy_stream));   // (async calls' copies)
   if ((s = ensure(h, h->stageA_d, sizeof(double) * h->nnz_A))) return s;
   if ((s = ensure(h, h->stageB_d, sizeof(double) * (size_t)h->n * R))) return s;
   if ((s = ensure(h, h->stageX_d, sizeof(double) * (size_t)h->W * R * h->n))) return s;

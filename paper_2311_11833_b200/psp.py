@@ -24,7 +24,7 @@ EXPORTS = ["psp_create", "psp_destroy", "psp_set_stream", "psp_status_string",
            "psp_last_error_detail", "psp_symbolic_analyse", "psp_get_symbolic_info",
            "psp_set_perturbations", "psp_factor_batch", "psp_solve_batch", "psp_factor_solve_batch",
            "psp_get_solutions", "psp_get_phase_times",
-           "psp_set_weights", "psp_recover", "psp_get_lane_status", "psp_solve_host",
+           "psp_set_weights", "psp_recover", "psp_get_lane_status", "psp_solve_host", "psp_solve_host_async",
            "psp_synchronize", "psp_ladder_weights", "psp_set_option", "psp_get_factor"]
 OPT = {"factor_groups": 1, "factor_warps": 2, "factor_lanes": 3, "factor_slab_warps": 4,
        "factor_pairs": 5, "factor_tmem": 6, "solve_tmem": 7, "phase_events": 8}
@@ -81,6 +81,7 @@ def lib():
             "psp_recover": [P, P],
             "psp_get_lane_status": [P, P],
             "psp_solve_host": [P, P, I32, P, D, P],
+            "psp_solve_host_async": [P, P, I32, P, D, P],
             "psp_ladder_weights": [I32, P, P, P],
             "psp_set_option": [P, I32, I64],
             "psp_get_factor": [P, I32, P],
@@ -247,6 +248,13 @@ class Solver:
             self._check(rc)
         self.R = R
         return rc
+
+    def psp_solve_host_async(self, A_vals_h, B_h, x_h, pivot_tol=0.0):
+        """Pipelined host-buffer call (pinned torch CPU tensors); psp_synchronize to wait."""
+        R = B_h.shape[0]
+        self._check(lib().psp_solve_host_async(self.h, _t_ptr(A_vals_h), R, _t_ptr(B_h),
+                                               float(pivot_tol), _t_ptr(x_h)))
+        self.R = R
 
     def psp_synchronize(self):
         self._check(lib().psp_synchronize(self.h))
