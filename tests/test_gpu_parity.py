@@ -154,6 +154,28 @@ def test_host_api_e2e_matches_device_path():
     assert np.array_equal(x_h.numpy(), g["xhat"])
 
 
+def test_host_api_async_pipeline():
+    """psp_solve_host_async: three back-to-back calls with different A values (the
+    double-buffered copies back overlap the next call) give, after psp_synchronize,
+    exactly what the synchronous psp_solve_host gives for each."""
+    w = config(1, n_ladders=4)
+    s = w.system()
+    eps = w.eps()
+    g = gpu_run(s, eps, ladders=w.ladders)
+    solver = g["solver"]
+    B_h = torch.tensor(s.b.T.copy(), dtype=torch.float64).pin_memory()
+    As = [torch.tensor(s.vals * f, dtype=torch.float64).pin_memory() for f in (1.0, 0.5, 2.0)]
+    xs = [torch.full((len(w.ladders), 1, s.n), np.nan, dtype=torch.float64).pin_memory() for _ in As]
+    for A_h, x_h in zip(As, xs):
+        solver.psp_solve_host_async(A_h, B_h, x_h)
+    solver.psp_synchronize()
+    for A_h, x_h in zip(As, xs):
+        ref = torch.empty_like(x_h).pin_memory()
+        assert solver.psp_solve_host(A_h, B_h, ref) == 0
+        assert np.array_equal(x_h.numpy(), ref.numpy())
+    assert np.array_equal(xs[0].numpy(), g["xhat"])
+
+
 @pytest.mark.parametrize("ci", [2])
 def test_cfg2_geometric_ladder_sampled(ci):
     w = config(ci)
