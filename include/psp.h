@@ -131,10 +131,12 @@ psp_status psp_destroy(psp_handle h);
  *                         (DESIGN.md §5).  Results are bitwise independent of it.
  *  PSP_OPT_PHASE_EVENTS   0 (default); 1: record CUDA events around the factor and the
  *                         solve kernel launches (for psp_get_phase_times; any time).
+ *  PSP_OPT_GROWTH         0 (default); 1: every factorisation also computes the per-lane
+ *                         growth factor (psp_get_lane_growth; any time).
  * Errors: ARG (STATE: PSP_OPT_PHASE_EVENTS on a host-only handle). */
 enum { PSP_OPT_FACTOR_GROUPS = 1, PSP_OPT_FACTOR_WARPS = 2, PSP_OPT_FACTOR_LANES = 3,
        PSP_OPT_FACTOR_SLAB_WARPS = 4, PSP_OPT_FACTOR_PAIRS = 5, PSP_OPT_FACTOR_TMEM = 6,
-       PSP_OPT_SOLVE_TMEM = 7, PSP_OPT_PHASE_EVENTS = 8 };
+       PSP_OPT_SOLVE_TMEM = 7, PSP_OPT_PHASE_EVENTS = 8, PSP_OPT_GROWTH = 9 };
 psp_status psp_set_option(psp_handle h, int32_t option, int64_t value);
 
 /* Rebind the handle to another stream of the same device. */
@@ -204,6 +206,14 @@ psp_status psp_solve_batch(psp_handle h, int32_t R, const double* B, int64_t ldb
  * factor configuration), ALLOC, CUDA. */
 psp_status psp_factor_solve_batch(psp_handle h, const double* A_vals, const double* b,
                                   double pivot_tol, int32_t* lane_status);
+
+/* Per-lane growth factor of the last factorisation made with PSP_OPT_GROWTH = 1
+ * (growth monitoring): growth_h[k] = max|U_k| / max|A_k| with
+ * A_k = A + eps_k D (its diagonal rounded as in the factorisation: a_ii + (eps_k d_i)),
+ * max|U_k| over the lane's upper factor including the pivots.  Synchronises.  For a
+ * failed lane (status != 0) the value covers the factor as computed.  Errors: ARG,
+ * STATE, CUDA. */
+psp_status psp_get_lane_growth(psp_handle h, double* growth_h);
 
 /* With PSP_OPT_PHASE_EVENTS on: device time (ms, cudaEventElapsedTime) of the last
  * factor kernel (ms_h[0]) and the last solve kernel (ms_h[1]) launched by the calls

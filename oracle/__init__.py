@@ -163,6 +163,36 @@ class SparseOracle:
                                   _p(Bc), float(tol), _p(X), _p(st))
         return X, st
 
+    def growth(self, eps, tol):
+        """Per-lane growth g_k = max|U_k| / max|A_k|: max over the
+        lane's filled U (pivots included) over max over A_k = A + eps_k D (diagonal
+        a_ii + (eps_k d_i), two roundings as in the factorisation).  NaN for a lane
+        whose pivot-free factorisation fails (the oracle stops at the failing pivot)."""
+        n = self.n
+        eps = np.asarray(eps, dtype=np.float64)
+        g = np.full(len(eps), np.nan)
+        upper = np.zeros(self.nnz_lu, dtype=bool)
+        for j in range(n):
+            upper[self.fcp[j]:self.fcp[j + 1]] = np.asarray(self.fri[self.fcp[j]:self.fcp[j + 1]]) <= j
+        for k, e in enumerate(eps):
+            fv, st = self.factor(float(e), tol)
+            if st:
+                continue
+            umax = float(np.max(np.abs(fv[: self.nnz_lu][upper])))
+            amax = 0.0
+            for j in range(n):
+                has_diag = False
+                for q in range(self.acp[j], self.acp[j + 1]):
+                    v = float(self.av[q])
+                    if self.ari[q] == j:
+                        v = v + float(np.float64(e) * self.dp[j])
+                        has_diag = True
+                    amax = max(amax, abs(v))
+                if not has_diag:
+                    amax = max(amax, abs(float(np.float64(e) * self.dp[j])))
+            g[k] = umax / amax
+        return g
+
     def factor(self, eps, tol):
         fv = np.empty(max(self.nnz_lu, 1))
         st = lib().oracle_sparse_lu(self.n, _p(self.acp), _p(self.ari), _p(self.av), _p(self.fcp),

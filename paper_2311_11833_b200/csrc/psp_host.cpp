@@ -69,6 +69,10 @@ struct psp_ctx {
   // PSP_OPT_PHASE_EVENTS: event pairs around every factor / solve kernel launch since
   // the last psp_get_phase_times (pools grow on demand, reused after a read)
   bool phase_events = false;
+  // PSP_OPT_GROWTH: per-lane growth g_k = max|U| / max|A_k| after every factorisation
+  bool growth = false;
+  DevBuf growth_d, offmax_d;
+  const uint8_t* isdiag_d = nullptr;   // plan buffer: CSR entry is a diagonal entry
   std::vector<cudaEvent_t> fev, sev;
   size_t nf = 0, ns = 0;
 
@@ -76,6 +80,7 @@ struct psp_ctx {
   int32_t K = 0, K_pad = 0;
   DevBuf eps_d, dperm_d, V_d, status_d, tol_d;
   bool factored = false;
+  bool growth_valid = false;
 
   // --- solve ---
   int32_t R = 0;
@@ -154,6 +159,7 @@ static void release_plan(psp_ctx* h) {
   for (auto& b : h->plan_bufs) b.release();
   h->plan_bufs.clear();
   h->plan = DevicePlan{};
+  h->isdiag_d = nullptr;
 }
 
 static void reset_numeric(psp_ctx* h) {
@@ -169,8 +175,10 @@ static void reset_numeric(psp_ctx* h) {
   h->wlane_d.release();
   h->wval_d.release();
   h->w_seg = false;
+  h->growth_d.release();
+  h->offmax_d.release();
   h->K = h->K_pad = h->R = h->W = 0;
-  h->factored = h->solved = h->recovered = false;
+  h->factored = h->solved = h->recovered = h->growth_valid = false;
 }
 
 extern "C" {
@@ -266,6 +274,10 @@ psp_status psp_set_option(psp_handle h, int32_t option, int64_t value) {
     case PSP_OPT_FACTOR_TMEM:
       if (value < 0 || value > 2) return fail(h, PSP_ERR_ARG, "PSP_OPT_FACTOR_TMEM must be 0, 1 or 2");
       h->opt_tmem = value;
+      return PSP_OK;
+    case PSP_OPT_GROWTH:
+      if (value != 0 && value != 1) return fail(h, PSP_ERR_ARG, "PSP_OPT_GROWTH must be 0 or 1");
+      h->growth = value != 0;
       return PSP_OK;
     case PSP_OPT_PHASE_EVENTS:
       if (value != 0 && value != 1) return fail(h, PSP_ERR_ARG, "PSP_OPT_PHASE_EVENTS must be 0 or 1");
@@ -508,6 +520,12 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
   }
   UP(acsc_ptr, acsc_ptr);
   UP(acsc_q, acsc_q);
+  {
+    std::vector<uint8_t> isdiag(std::max(nnzA, 1), 0);
+    for (int32_t r = 0; r < n; ++r)
+      for (int32_t q = row_ptr_h[r]; q < row_ptr_h[r + 1]; ++q) isdiag[q] = col_idx_h[q] == r;
+    if (!host_only && (s = upload(h, isdiag, &h->isdiag_d))) return s;
+  }
 #undef UP
   if (!psp::choose_launch(P, h->launch, (int)h->opt_groups, (int)h->opt_warps,
                           (int)h->opt_lanes, (int)h->opt_slab_warps, (int)h->opt_tmem,
@@ -689,6 +707,11 @@ static psp_status factor_impl(psp_handle h, const double* A_vals, double pivot_t
   if (h->phase_events) {
     if ((s = phase_mark(h, h->fev, h->nf))) return s;
   }
+  if (h->growth && h->growth_d.bytes < sizeof(double) * (size_t)h->K_pad) {
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    if ((s = ensure(h, h->growth_d, sizeof(double) * (size_t)h->K_pad))) return s;
+    if ((s = ensure(h, h->offmax_d, sizeof(double)))) return s;
+  }
   CUDA_TRY(h, psp::launch_factor(P, LI, P.f_stream, (const double*)h->eps_d.p, tol_dev, pivot_tol,
                                  (double*)h->V_d.p, (double*)h->fscratch_d.p, (double*)h->fscr_d.p,
                                  (int32_t*)h->status_d.p, h->K_pad,
@@ -696,6 +719,11 @@ static psp_status factor_impl(psp_handle h, const double* A_vals, double pivot_t
   if (h->phase_events) {
     if ((s = phase_mark(h, h->fev, h->nf))) return s;
   }
+  if (h->growth)
+    CUDA_TRY(h, psp::launch_growth(P, LI, (const double*)h->V_d.p, A_vals, h->isdiag_d,
+                                   (const double*)h->eps_d.p, (const double*)h->dperm_d.p, h->K,
+                                   (double*)h->offmax_d.p, (double*)h->growth_d.p, h->stream));
+  h->growth_valid = h->growth;
   if (lane_status)
     CUDA_TRY(h, cudaMemcpyAsync(lane_status, h->status_d.p, sizeof(int32_t) * h->K,
                                 cudaMemcpyDeviceToDevice, h->stream));
@@ -767,6 +795,15 @@ psp_status psp_solve_batch(psp_handle h, int32_t R, const double* B, int64_t ldb
   }
   h->R = R;
   h->solved = true;
+  return PSP_OK;
+}
+
+psp_status psp_get_lane_growth(psp_handle h, double* growth_h) {
+  if (!h || !growth_h) return PSP_ERR_ARG;
+  if (!h->growth_valid) return fail(h, PSP_ERR_STATE, "factor with PSP_OPT_GROWTH = 1 first");
+  cudaSetDevice(h->device);
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  CUDA_TRY(h, cudaMemcpy(growth_h, h->growth_d.p, sizeof(double) * h->K, cudaMemcpyDeviceToHost));
   return PSP_OK;
 }
 

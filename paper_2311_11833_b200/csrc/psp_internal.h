@@ -100,6 +100,10 @@ cudaError_t launch_factor(const DevicePlan& p, const LaunchInfo& li, const int32
                           const double* eps, const double* tol_dev, double tol_value, double* V,
                           double* gscratch, double* gscr, int32_t* status, int32_t K_pad,
                           double* Y, cudaStream_t stream);
+// g_k = max|U| / max|A_k| per lane, from the factor in V (growth monitoring)
+cudaError_t launch_growth(const DevicePlan& p, const LaunchInfo& li, const double* V, const double* A,
+                          const uint8_t* isdiag, const double* eps, const double* dperm, int32_t K,
+                          double* offmax_scratch, double* growth, cudaStream_t stream);
 cudaError_t launch_solve(const DevicePlan& p, const LaunchInfo& li, const double* V,
                          const double* B, int64_t ldb, int32_t R, double* X, double* gscratch,
                          int32_t K_pad, bool forward, cudaStream_t stream);

@@ -23,11 +23,11 @@ ORDER = {"natural": 0, "mindeg": 1, "user": 2, "mindeg_first": 3}
 EXPORTS = ["psp_create", "psp_destroy", "psp_set_stream", "psp_status_string",
            "psp_last_error_detail", "psp_symbolic_analyse", "psp_get_symbolic_info",
            "psp_set_perturbations", "psp_factor_batch", "psp_solve_batch", "psp_factor_solve_batch",
-           "psp_get_solutions", "psp_get_phase_times",
+           "psp_get_solutions", "psp_get_phase_times", "psp_get_lane_growth",
            "psp_set_weights", "psp_recover", "psp_get_lane_status", "psp_solve_host", "psp_solve_host_async",
            "psp_synchronize", "psp_ladder_weights", "psp_set_option", "psp_get_factor"]
 OPT = {"factor_groups": 1, "factor_warps": 2, "factor_lanes": 3, "factor_slab_warps": 4,
-       "factor_pairs": 5, "factor_tmem": 6, "solve_tmem": 7, "phase_events": 8}
+       "factor_pairs": 5, "factor_tmem": 6, "solve_tmem": 7, "phase_events": 8, "growth": 9}
 
 
 class SymbolicInfo(ctypes.Structure):
@@ -76,6 +76,7 @@ def lib():
             "psp_solve_batch": [P, I32, P, I64],
             "psp_factor_solve_batch": [P, P, P, D, P],
             "psp_get_phase_times": [P, P],
+            "psp_get_lane_growth": [P, P],
             "psp_get_solutions": [P, P],
             "psp_set_weights": [P, I32, P, P, P],
             "psp_recover": [P, P],
@@ -201,6 +202,12 @@ class Solver:
             ls = _t_ptr(lane_status)
         self._check(lib().psp_factor_solve_batch(self.h, _t_ptr(A_vals), _t_ptr(b), float(pivot_tol), ls))
         self.R = 1
+
+    def psp_get_lane_growth(self):
+        """g_k = max|U_k| / max|A_k| of the last factorisation (growth option on)."""
+        g = np.empty(self.K, dtype=np.float64)
+        self._check(lib().psp_get_lane_growth(self.h, _np_ptr(g)))
+        return g
 
     def psp_get_phase_times(self):
         """(factor_ms, solve_ms) of the last factor / solve kernels (phase_events on)."""

@@ -376,6 +376,39 @@ def test_fused_factor_solve_bitwise(ci, K):
     assert all(np.array_equal(f1, f2) for f1, f2 in zip(F, outs[1][2]))
 
 
+@pytest.mark.parametrize("fused", [False, True])
+def test_lane_growth_matches_oracle(fused):
+    """PSP_OPT_GROWTH: per-lane g_k = max|U_k| / max|A_k| computed on the device after
+    the factorisation (a pass over the DU region of the factor) equals the oracle's
+    exactly (max and one division), in both
+    the plain and the fused factorisation; the option leaves the solutions unchanged."""
+    s = config(1).system()
+    rng = np.random.default_rng(5)
+    K = 70
+    eps = rng.choice([-1, 1], K) * 10.0 ** rng.uniform(-6, -2, K)
+    A = torch.tensor(s.vals, dtype=torch.float64, device="cuda")
+    b = torch.tensor(s.b[:, 0].copy(), dtype=torch.float64, device="cuda")
+    Xs = []
+    for grow in (1, 0):
+        solver = psp.Solver(0)
+        solver.psp_set_option("growth", grow)
+        solver.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering="mindeg")
+        info, perm = solver.psp_get_symbolic_info()
+        solver.psp_set_perturbations(eps, s.d)
+        if fused:
+            solver.psp_factor_solve_batch(A, b, 1e-300)
+        else:
+            solver.psp_factor_batch(A, 1e-300)
+            solver.psp_solve_batch(b.view(1, -1))
+        Xs.append(solver.psp_get_solutions().cpu().numpy())
+        if grow:
+            g = solver.psp_get_lane_growth()
+            go = oracle.SparseOracle(s, perm).growth(eps[:12], 1e-300)
+            assert np.array_equal(g[:12], go)
+            assert np.all(np.isfinite(g)) and np.all(g > 0)
+    assert np.array_equal(Xs[0], Xs[1])
+
+
 def test_sharded_recover_partials_sum_to_full():
     """Row a6 on one GPU: lanes split over two handles (a ladder straddles the split);
     each recovers its partial sums with its shard of the weights; their sum equals the

@@ -272,3 +272,20 @@ def test_postorder_is_topological_and_keeps_fill(ci):
         below = rows[rows > j]
         if len(below):
             assert below.min() > j
+
+
+def test_growth_pins():
+    """Oracle growth g_k = max|U_k| / max|A_k|: a diagonal matrix
+    factors to itself (g = 1 exactly, any eps); [[delta, 1], [1, 1]] with delta = 2^-10
+    has U = [[delta, 1], [0, 1 - 1/delta]], so g = 1023 exactly at eps = 0; with eps the
+    perturbed pivot delta + eps enters both U and A_k."""
+    A = np.diag([2.0, -3.0, 0.5, 4.0])
+    so = oracle.SparseOracle(_Tiny(A, [1.0, -0.5, 0.25, 1.0], np.ones(4)), np.arange(4, dtype=np.int32))
+    assert np.array_equal(so.growth([0.0, 1e-3, -0.25], 1e-300), [1.0, 1.0, 1.0])
+    delta = 2.0 ** -10
+    A2 = np.array([[delta, 1.0], [1.0, 1.0]])
+    so2 = oracle.SparseOracle(_Tiny(A2, [1.0, 0.0], np.ones(2)), np.arange(2, dtype=np.int32))
+    g = so2.growth([0.0, 2.0 ** -10], 1e-300)
+    assert g[0] == 1023.0
+    p = delta + 2.0 ** -10                       # = 2^-9, exact
+    assert g[1] == abs(1.0 - 1.0 / p) / 1.0      # |u_22| = 511 > 1 = max|A_k|
