@@ -21,7 +21,7 @@ constexpr int kFMaxStages = 8;        // factor ring: 4 or 8 stages (LaunchInfo:
 constexpr int kYRows = 16;            // y rows per stage of the solve's y ring
 constexpr int kDataStages = 2;        // depth of the solve's per-warp factor-row ring
 constexpr int kSolveMaxC = 16;        // records with c <= kSolveMaxC take the unrolled path
-constexpr int kMaxWarpsCta = 16;      // consumer warps per CTA (plus one producer warp)
+constexpr int kMaxWarpsCta = 16;      // warps per CTA (all consumers: self-refilling ring)
 constexpr int kFusedMax = 12;         // pivots with c <= kFusedMax: u in registers, no scratch
 constexpr int kPairMax = 8;          // supernode pairs for c <= kPairMax
 
