@@ -207,6 +207,21 @@ psp_status psp_solve_batch(psp_handle h, int32_t R, const double* B, int64_t ldb
 psp_status psp_factor_solve_batch(psp_handle h, const double* A_vals, const double* b,
                                   double pivot_tol, int32_t* lane_status);
 
+/* Spectral radius rho(A^-1 D) by power iteration (Eq. (4)'s rho; the convergence
+ * premise eps_c = m eps < 1 / rho of Theorem 1),
+ * reusing the handle's factorisation: A^-1 r is applied as the recovered solution w of
+ * the method itself (psp_solve_batch with R = 1 and b = r, psp_recover, row w), so it
+ * carries the method's O(eps^2m) truncation error.  v_0 = v0_h (n values, ORIGINAL
+ * ordering, nonzero); v_{t+1} = x_hat(D v_t) / ||x_hat(D v_t)||_2, rho_t = ||x_hat(D v_t)||_2
+ * (||v_t||_2 = 1); stops when |rho_t - rho_{t-1}| < rtol * rho_t or after max_iter
+ * iterations.  Outputs rho_h, iters_h (may be NULL), converged_h (1 / 0, may be NULL).
+ * Overwrites the solutions and the recovered rows of the handle (the last iterate).
+ * Synchronous.  Errors: ARG, STATE (factor_batch and set_weights first),
+ * BATCH_INFEASIBLE (non-finite iterate), CUDA. */
+psp_status psp_estimate_rho(psp_handle h, int32_t w, int32_t max_iter, double rtol,
+                            const double* v0_h, double* rho_h, int32_t* iters_h,
+                            int32_t* converged_h);
+
 /* Per-lane growth factor of the last factorisation made with PSP_OPT_GROWTH = 1
  * (growth monitoring): growth_h[k] = max|U_k| / max|A_k| with
  * A_k = A + eps_k D (its diagonal rounded as in the factorisation: a_ii + (eps_k d_i)),

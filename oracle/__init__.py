@@ -112,6 +112,33 @@ def lu_pp_solve(LU, piv, b):
     return y
 
 
+def power_rho(sysm, v0, max_iter=500, rtol=1e-6):
+    """rho(A^-1 D) by power iteration on v -> A^-1 (D v) with A^-1 applied through a
+    partial-pivot LU (Eq. (4)): v_0 = v0 / ||v0||_2,
+    rho_t = ||A^-1 D v_t||_2, v_{t+1} = A^-1 D v_t / rho_t, stop when
+    |rho_t - rho_{t-1}| < rtol * rho_t.  Returns (rho, iterations, converged)."""
+    n = sysm.n
+    A = np.zeros((n, n))
+    for i in range(n):
+        for q in range(sysm.row_ptr[i], sysm.row_ptr[i + 1]):
+            A[i, sysm.col_idx[q]] += sysm.vals[q]
+    LU, piv, st = lu_partial_pivot(A)
+    if st:
+        raise ValueError("singular A")
+    d = np.asarray(sysm.d, dtype=np.float64)
+    v = np.asarray(v0, dtype=np.float64) / np.linalg.norm(v0)
+    rho, it = 0.0, 0
+    for it in range(1, max_iter + 1):
+        u = lu_pp_solve(LU, piv, d * v)
+        prev, rho = rho, float(np.linalg.norm(u))
+        if rho == 0.0:
+            return rho, it, False
+        v = u / rho
+        if it > 1 and abs(rho - prev) < rtol * rho:
+            return rho, it, True
+    return rho, max_iter, False
+
+
 def default_tol(n, row_ptr, col_idx, vals):
     """zero_tol = n * u * ||A||_1 of the unperturbed A (reading R10)."""
     cs = np.zeros(n)

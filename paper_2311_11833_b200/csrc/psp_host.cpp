@@ -81,6 +81,8 @@ struct psp_ctx {
   DevBuf eps_d, dperm_d, V_d, status_d, tol_d;
   bool factored = false;
   bool growth_valid = false;
+  std::vector<double> d_host;   // D's diagonal, original ordering (psp_estimate_rho)
+  DevBuf rho_r_d, rho_x_d;      // psp_estimate_rho: right-hand side D v, recovered rows
 
   // --- solve ---
   int32_t R = 0;
@@ -637,6 +639,7 @@ psp_status psp_set_perturbations(psp_handle h, int32_t K, const double* eps_h, c
   CUDA_TRY(h, cudaMemset(h->flag_d.p, 0, sizeof(int32_t)));
   h->K = K;
   h->K_pad = Kp;
+  h->d_host.assign(d_h, d_h + h->n);
   h->factored = h->solved = h->recovered = false;
   return PSP_OK;
 }
@@ -795,6 +798,56 @@ psp_status psp_solve_batch(psp_handle h, int32_t R, const double* B, int64_t ldb
   }
   h->R = R;
   h->solved = true;
+  return PSP_OK;
+}
+
+psp_status psp_estimate_rho(psp_handle h, int32_t w, int32_t max_iter, double rtol,
+                            const double* v0_h, double* rho_h, int32_t* iters_h,
+                            int32_t* converged_h) {
+  if (!h || !v0_h || !rho_h || max_iter < 1 || !(rtol > 0)) return PSP_ERR_ARG;
+  if (!h->factored || h->W == 0) return fail(h, PSP_ERR_STATE, "factor_batch and set_weights first");
+  if (w < 0 || w >= h->W) return fail(h, PSP_ERR_ARG, "w out of range");
+  const int32_t n = h->n;
+  cudaSetDevice(h->device);
+  psp_status s;
+  if ((s = ensure(h, h->rho_r_d, sizeof(double) * n))) return s;
+  if ((s = ensure(h, h->rho_x_d, sizeof(double) * (size_t)h->W * n))) return s;
+  // v = v0 / ||v0||_2
+  std::vector<double> v(v0_h, v0_h + n), r(n), u(n);
+  auto nrm = [&](const std::vector<double>& x) {
+    long double a = 0;
+    for (double t : x) a += (long double)t * t;
+    return (double)std::sqrt(a);
+  };
+  double nv = nrm(v);
+  if (!(nv > 0) || !std::isfinite(nv)) return fail(h, PSP_ERR_ARG, "v0 must be nonzero and finite");
+  for (double& t : v) t /= nv;
+  double rho = 0.0;
+  int32_t it = 0, conv = 0;
+  for (it = 1; it <= max_iter; ++it) {
+    for (int32_t i = 0; i < n; ++i) r[i] = h->d_host[i] * v[i];   // r = D v
+    CUDA_TRY(h, cudaMemcpyAsync(h->rho_r_d.p, r.data(), sizeof(double) * n, cudaMemcpyHostToDevice,
+                                h->stream));
+    if ((s = psp_solve_batch(h, 1, (const double*)h->rho_r_d.p, n))) return s;
+    if ((s = psp_recover(h, (double*)h->rho_x_d.p))) return s;
+    CUDA_TRY(h, cudaMemcpyAsync(u.data(), (const double*)h->rho_x_d.p + (size_t)w * n,
+                                sizeof(double) * n, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    const double nu = nrm(u);   // ||x-hat(D v)|| with ||v|| = 1
+    if (!std::isfinite(nu))
+      return fail(h, PSP_ERR_BATCH_INFEASIBLE, "non-finite iterate (a weight on a failed lane)");
+    const double prev = rho;
+    rho = nu;
+    if (nu == 0.0) break;
+    for (int32_t i = 0; i < n; ++i) v[i] = u[i] / nu;
+    if (it > 1 && std::fabs(rho - prev) < rtol * rho) {
+      conv = 1;
+      break;
+    }
+  }
+  *rho_h = rho;
+  if (iters_h) *iters_h = std::min(it, max_iter);
+  if (converged_h) *converged_h = conv;
   return PSP_OK;
 }
 

@@ -23,7 +23,7 @@ ORDER = {"natural": 0, "mindeg": 1, "user": 2, "mindeg_first": 3}
 EXPORTS = ["psp_create", "psp_destroy", "psp_set_stream", "psp_status_string",
            "psp_last_error_detail", "psp_symbolic_analyse", "psp_get_symbolic_info",
            "psp_set_perturbations", "psp_factor_batch", "psp_solve_batch", "psp_factor_solve_batch",
-           "psp_get_solutions", "psp_get_phase_times", "psp_get_lane_growth",
+           "psp_get_solutions", "psp_get_phase_times", "psp_get_lane_growth", "psp_estimate_rho",
            "psp_set_weights", "psp_recover", "psp_get_lane_status", "psp_solve_host", "psp_solve_host_async",
            "psp_synchronize", "psp_ladder_weights", "psp_set_option", "psp_get_factor"]
 OPT = {"factor_groups": 1, "factor_warps": 2, "factor_lanes": 3, "factor_slab_warps": 4,
@@ -77,6 +77,7 @@ def lib():
             "psp_factor_solve_batch": [P, P, P, D, P],
             "psp_get_phase_times": [P, P],
             "psp_get_lane_growth": [P, P],
+            "psp_estimate_rho": [P, I32, I32, D, P, P, P, P],
             "psp_get_solutions": [P, P],
             "psp_set_weights": [P, I32, P, P, P],
             "psp_recover": [P, P],
@@ -202,6 +203,18 @@ class Solver:
             ls = _t_ptr(lane_status)
         self._check(lib().psp_factor_solve_batch(self.h, _t_ptr(A_vals), _t_ptr(b), float(pivot_tol), ls))
         self.R = 1
+
+    def psp_estimate_rho(self, w=0, max_iter=500, rtol=1e-6, v0=None):
+        """rho(A^-1 D) by power iteration through recovered solution w (psp.h).
+        Returns (rho, iterations, converged)."""
+        v = np.ones(self.n) if v0 is None else np.ascontiguousarray(v0, dtype=np.float64)
+        rho = ctypes.c_double()
+        it = ctypes.c_int32()
+        conv = ctypes.c_int32()
+        self._check(lib().psp_estimate_rho(self.h, int(w), int(max_iter), float(rtol), _np_ptr(v),
+                                           ctypes.byref(rho), ctypes.byref(it), ctypes.byref(conv)))
+        self.R = 1
+        return rho.value, it.value, bool(conv.value)
 
     def psp_get_lane_growth(self):
         """g_k = max|U_k| / max|A_k| of the last factorisation (growth option on)."""

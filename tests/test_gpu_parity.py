@@ -409,6 +409,39 @@ def test_lane_growth_matches_oracle(fused):
     assert np.array_equal(Xs[0], Xs[1])
 
 
+def test_estimate_rho_matches_oracle_power_iteration():
+    """psp_estimate_rho: power iteration for rho(A^-1 D) through the method's own
+    recovered solutions (one alpha = 1..4 ladder at eps = 2e-3; eps_c * rho ~ 0.01, so
+    the truncation error is ~1e-16) against the oracle's power iteration with a
+    partial-pivot A^-1, same start vector and stopping rule; and a diagonal system's
+    closed form max|d_i / a_i|."""
+    w = config(1, n_ladders=1)
+    s = w.system()
+    eps = w.eps()
+    g = gpu_run(s, eps, ladders=w.ladders)
+    rho, it, conv = g["solver"].psp_estimate_rho(0, 500, 1e-6)
+    ro, ito, convo = oracle.power_rho(s, np.ones(s.n), 500, 1e-6)
+    assert conv and convo
+    assert abs(rho - ro) <= 1e-5 * ro
+    assert np.max(np.abs(eps)) * rho < 1.0   # Theorem 1's premise eps_c * rho < 1 (P:L122)
+    # diagonal: A^-1 D is diagonal, rho = max |d_i / a_i|
+    rng = np.random.default_rng(11)
+    n = 40
+    a = rng.uniform(1, 3, n) * rng.choice([-1, 1], n)
+    d = rng.uniform(-1, 1, n)
+    a[5], d[5] = 0.25, 1.0
+    class _Diag:
+        pass
+    sd = _Diag()
+    sd.n, sd.row_ptr, sd.col_idx, sd.vals = n, np.arange(n + 1, dtype=np.int32), np.arange(n, dtype=np.int32), a
+    sd.d, sd.b = d, np.ones((n, 1))
+    ladder = [np.array([1e-5, 2e-5])]
+    eps_d = psp.psp_ladder_weights(ladder[0])[0]
+    gd = gpu_run(sd, eps_d, ordering_kind="natural", ladders=ladder)
+    rho_d, _, conv_d = gd["solver"].psp_estimate_rho(0, 500, 1e-12)
+    assert conv_d and abs(rho_d - np.max(np.abs(d / a))) <= 1e-9 * 4
+
+
 def test_sharded_recover_partials_sum_to_full():
     """Row a6 on one GPU: lanes split over two handles (a ladder straddles the split);
     each recovers its partial sums with its shard of the weights; their sum equals the

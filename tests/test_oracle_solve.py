@@ -289,3 +289,28 @@ def test_growth_pins():
     assert g[0] == 1023.0
     p = delta + 2.0 ** -10                       # = 2^-9, exact
     assert g[1] == abs(1.0 - 1.0 / p) / 1.0      # |u_22| = 511 > 1 = max|A_k|
+
+
+def test_power_rho_pins():
+    """Oracle rho(A^-1 D) by power iteration: the SPEC's worked values
+    (diag(2,4), D = I -> 0.5; [[2,1],[1,2]], D = I -> 1), a diagonal closed form
+    max|d_i / a_i|, and the largest |eigenvalue| of A^-1 D from LAPACK's eig on a
+    random well-separated system."""
+    r, it, conv = oracle.power_rho(_Tiny(np.diag([2.0, 4.0]), [1.0, 1.0], [1.0, 1.0]), [1.0, 1.0])
+    assert conv and abs(r - 0.5) < 1e-6
+    r, it, conv = oracle.power_rho(_Tiny(np.array([[2.0, 1.0], [1.0, 2.0]]), [1.0, 1.0], [1.0, 1.0]),
+                                   [1.0, 0.3])
+    assert conv and abs(r - 1.0) < 1e-6
+    rng = np.random.default_rng(3)
+    a = rng.uniform(1, 3, 40) * rng.choice([-1, 1], 40)
+    d = rng.uniform(-1, 1, 40)
+    d[7] = 1.0
+    a[7] = 0.25   # dominant ratio 4, the next one < 1
+    r, it, conv = oracle.power_rho(_Tiny(np.diag(a), d, np.ones(40)), np.ones(40), rtol=1e-12)
+    assert conv and abs(r - np.max(np.abs(d / a))) <= 1e-12 * 4
+    n = 12
+    M = rng.normal(size=(n, n)) + 4 * np.eye(n)
+    dd = rng.uniform(0.2, 1.0, n)
+    lam = np.max(np.abs(np.linalg.eigvals(np.linalg.solve(M, np.diag(dd)))))
+    r, it, conv = oracle.power_rho(_Tiny(M, dd, np.ones(n)), np.ones(n), max_iter=5000, rtol=1e-13)
+    assert abs(r - lam) <= 1e-8 * lam
