@@ -442,6 +442,51 @@ def test_estimate_rho_matches_oracle_power_iteration():
     assert conv_d and abs(rho_d - np.max(np.abs(d / a))) <= 1e-9 * 4
 
 
+@pytest.mark.parametrize("n", [1, 2, 40])
+def test_degenerate_patterns_fused_and_separate(n):
+    """Degenerate shapes through both paths: n = 1 (one pivot, empty L), a 2 x 2 with a
+    zero diagonal entry (the method's leading-zero regime in miniature), and a diagonal
+    n = 40 (every pivot with c = 0: births and pivots only); K = 33 (ragged)."""
+    rng = np.random.default_rng(n)
+    if n == 2:
+        Ad = np.array([[0.0, 1.5], [2.0, 1.0]])
+    else:
+        Ad = np.diag(rng.uniform(1, 3, n) * rng.choice([-1, 1], n))
+
+    class _S:
+        pass
+    s = _S()
+    rp, ci, v = [0], [], []
+    for i in range(n):
+        for j in range(n):
+            if Ad[i, j] != 0 or i == j:
+                ci.append(j)
+                v.append(Ad[i, j])
+        rp.append(len(ci))
+    s.n, s.row_ptr, s.col_idx, s.vals = n, np.array(rp, np.int32), np.array(ci, np.int32), np.array(v)
+    s.d = np.where(np.arange(n) % 2 == 0, 1.0, -0.5)
+    s.b = rng.normal(size=(n, 1))
+    K = 33
+    eps = rng.choice([-1, 1], K) * 10.0 ** rng.uniform(-4, -1, K)
+    A = torch.tensor(s.vals, dtype=torch.float64, device="cuda")
+    b = torch.tensor(s.b[:, 0].copy(), dtype=torch.float64, device="cuda")
+    outs = []
+    for fused in (True, False):
+        solver = psp.Solver(0)
+        solver.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering="natural")
+        info, perm = solver.psp_get_symbolic_info()
+        solver.psp_set_perturbations(eps, s.d)
+        if fused:
+            solver.psp_factor_solve_batch(A, b, 1e-300)
+        else:
+            solver.psp_factor_batch(A, 1e-300)
+            solver.psp_solve_batch(b.view(1, -1))
+        outs.append(solver.psp_get_solutions().cpu().numpy())
+    Xo, sto = oracle.SparseOracle(s, np.arange(n, dtype=np.int32)).batch(eps, 1e-300)
+    assert np.all(sto == 0)
+    assert np.array_equal(outs[0], Xo) and np.array_equal(outs[1], Xo)
+
+
 def test_sharded_recover_partials_sum_to_full():
     """Row a6 on one GPU: lanes split over two handles (a ladder straddles the split);
     each recovers its partial sums with its shard of the weights; their sum equals the
