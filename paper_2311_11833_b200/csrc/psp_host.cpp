@@ -646,9 +646,9 @@ psp_status psp_set_perturbations(psp_handle h, int32_t K, const double* eps_h, c
 
 // The solve's launch configuration for this batch: the TMEM one when it needs fewer
 // waves (rounds of resident warps over the SMs), else the shared-memory one.
-static const psp::LaunchInfo& solve_launch(psp_ctx* h) {
+static const psp::LaunchInfo& solve_launch(psp_ctx* h, int32_t R = 1) {
   if (!h->stm_ok) return h->launch;
-  const int64_t blocks = h->K_pad / psp::kBlock;
+  const int64_t blocks = h->K_pad / psp::kBlock * (R > 1 ? R : 1);   // (R-parallel items)
   auto rounds = [&](const psp::LaunchInfo& li) {
     const int64_t per = (int64_t)li.s_warps * std::max(1, li.s_ctas_per_sm) * h->n_sm;
     return (blocks + per - 1) / per;
@@ -740,10 +740,11 @@ psp_status psp_factor_batch(psp_handle h, const double* A_vals, double pivot_tol
   return factor_impl(h, A_vals, pivot_tol, lane_status, false, nullptr);
 }
 
-static psp_status solve_scratch(psp_handle h) {
+static psp_status solve_scratch(psp_handle h, int32_t R) {
   psp_status s;
-  if (!solve_launch(h).s_live_smem) {
-    size_t need2 = sizeof(double) * (size_t)h->K_pad * (h->plan.y_slots + h->plan.x_slots + 1);
+  if (!solve_launch(h, R).s_live_smem) {   // (R-parallel solves: one live set per RHS)
+    size_t need2 = sizeof(double) * (size_t)h->K_pad * (h->plan.y_slots + h->plan.x_slots + 1) *
+                   (size_t)(R > 1 ? R : 1);
     if (h->sscratch_d.bytes < need2) {
       CUDA_TRY(h, cudaStreamSynchronize(h->stream));
       if ((s = ensure(h, h->sscratch_d, need2))) return s;
@@ -760,7 +761,7 @@ psp_status psp_factor_solve_batch(psp_handle h, const double* A_vals, const doub
     return fail(h, PSP_ERR_UNSUPPORTED, "no factor configuration fits the augmented program");
   psp_status s = factor_impl(h, A_vals, pivot_tol, lane_status, true, b);
   if (s) return s;
-  if ((s = solve_scratch(h))) return s;
+  if ((s = solve_scratch(h, 1))) return s;
   if (h->phase_events) {
     if ((s = phase_mark(h, h->sev, h->ns))) return s;
   }
@@ -786,11 +787,11 @@ psp_status psp_solve_batch(psp_handle h, int32_t R, const double* B, int64_t ldb
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     if ((s = ensure(h, h->X_d, need))) return s;
   }
-  if ((s = solve_scratch(h))) return s;
+  if ((s = solve_scratch(h, R))) return s;
   if (h->phase_events) {
     if ((s = phase_mark(h, h->sev, h->ns))) return s;
   }
-  CUDA_TRY(h, psp::launch_solve(h->plan, solve_launch(h), (const double*)h->V_d.p, B, ldb, R,
+  CUDA_TRY(h, psp::launch_solve(h->plan, solve_launch(h, R), (const double*)h->V_d.p, B, ldb, R,
                                 (double*)h->X_d.p, (double*)h->sscratch_d.p, h->K_pad, true,
                                 h->stream));
   if (h->phase_events) {
