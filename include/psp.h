@@ -94,7 +94,8 @@ typedef struct {
                                     shared memory (PSP_OPT_FACTOR_TMEM)               */
   int32_t solve_live_smem;       /* 1: solve's live slots in shared memory, 0: global,
                                     2: tensor memory (PSP_OPT_SOLVE_TMEM)             */
-  /* the augmented program of psp_factor_solve_batch ([A | b]; aug_ok = 0: unavailable) */
+  /* the augmented program of psp_factor_solve_batch ([A | b]): aug_ok = 2 fused, 1
+   * available but slower (a weaker slot store: the call runs factor + solve), 0 none */
   int32_t aug_ok, aug_max_live, aug_warps_per_cta, aug_pend_smem;
 } psp_symbolic_info;
 
@@ -202,8 +203,9 @@ psp_status psp_solve_batch(psp_handle h, int32_t R, const double* B, int64_t ldb
  * pass would, and the solve runs the backward pass only.  Results (factor, lane
  * statuses, solutions) are bitwise those of psp_factor_batch + psp_solve_batch with
  * R = 1.  Saves the forward pass's read of L and its interpretation overhead
- * (DESIGN.md §5).  Errors: ARG, STATE, UNSUPPORTED (the augmented program fits no
- * factor configuration), ALLOC, CUDA. */
+ * (DESIGN.md §5).  When the augmented program would need a weaker pending-slot store
+ * than the plain one (symbolic info aug_ok != 2) it runs psp_factor_batch +
+ * psp_solve_batch instead.  Errors: ARG, STATE, ALLOC, CUDA. */
 psp_status psp_factor_solve_batch(psp_handle h, const double* A_vals, const double* b,
                                   double pivot_tol, int32_t* lane_status);
 

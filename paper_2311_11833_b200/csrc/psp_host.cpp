@@ -60,6 +60,9 @@ struct psp_ctx {
   DevicePlan plan_aug;
   psp::LaunchInfo launch_aug;
   bool aug_ok = false;
+  bool aug_fast = false;   // the augmented program keeps the plain one's slot store (TMEM /
+                           // shared / global): psp_factor_solve_batch fuses, else it runs
+                           // the two calls (measured: a store downgrade costs more)
   int64_t opt_groups = 0, opt_warps = 0, opt_lanes = 0, opt_slab_warps = 0;  // PSP_OPT_FACTOR_*
   int64_t opt_pairs = 1;                                                      // PSP_OPT_FACTOR_PAIRS
   int64_t opt_tmem = 0;                                                       // PSP_OPT_FACTOR_TMEM
@@ -354,7 +357,7 @@ psp_status psp_solve_host_async(psp_handle h, const double* A_vals_h, int32_t R,
                               cudaMemcpyHostToDevice, h->stream));
   CUDA_TRY(h, cudaMemcpyAsync(h->stageB_d.p, B_h, sizeof(double) * (size_t)h->n * R,
                               cudaMemcpyHostToDevice, h->stream));
-  if (R == 1 && h->aug_ok) {
+  if (R == 1) {
     if ((s = psp_factor_solve_batch(h, (const double*)h->stageA_d.p, (const double*)h->stageB_d.p,
                                     pivot_tol, nullptr)))
       return s;
@@ -567,6 +570,10 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
   }
   h->plan_aug = Pa;
   h->launch_aug = la;
+  {
+    auto store = [](const psp::LaunchInfo& li) { return li.f_tmem ? 2 : (li.f_pend_smem ? 1 : 0); };
+    h->aug_fast = h->aug_ok && store(la) == store(h->launch);
+  }
   h->plan = P;
   h->perm = perm;
   h->n = n;
@@ -606,7 +613,7 @@ psp_status psp_get_symbolic_info(psp_handle h, psp_symbolic_info* info, int32_t*
   info->factor_pend_smem = h->launch.f_tmem ? 2 : (h->launch.f_pend_smem ? 1 : 0);
   info->solve_live_smem = h->launch.s_tmem ? 2 : (h->launch.s_live_smem ? 1 : 0);
   info->solve_live = h->y_slots + h->x_slots;
-  info->aug_ok = h->aug_ok ? 1 : 0;
+  info->aug_ok = h->aug_fast ? 2 : (h->aug_ok ? 1 : 0);
   info->aug_max_live = h->plan_aug.f_slots;
   info->aug_warps_per_cta = h->aug_ok ? h->launch_aug.f_warps : 0;
   info->aug_pend_smem = !h->aug_ok ? 0 : (h->launch_aug.f_tmem ? 2 : (h->launch_aug.f_pend_smem ? 1 : 0));
@@ -757,9 +764,12 @@ psp_status psp_factor_solve_batch(psp_handle h, const double* A_vals, const doub
                                   double pivot_tol, int32_t* lane_status) {
   if (!h) return PSP_ERR_ARG;
   if (!b) return fail(h, PSP_ERR_ARG, "b required");
-  if (h->analysed && !h->aug_ok)
-    return fail(h, PSP_ERR_UNSUPPORTED, "no factor configuration fits the augmented program");
-  psp_status s = factor_impl(h, A_vals, pivot_tol, lane_status, true, b);
+  psp_status s;
+  if (h->analysed && !h->aug_fast) {   // the two calls (bitwise the same results)
+    if ((s = factor_impl(h, A_vals, pivot_tol, lane_status, false, nullptr))) return s;
+    return psp_solve_batch(h, 1, b, h->n);
+  }
+  s = factor_impl(h, A_vals, pivot_tol, lane_status, true, b);
   if (s) return s;
   if ((s = solve_scratch(h, 1))) return s;
   if (h->phase_events) {
@@ -1000,7 +1010,7 @@ psp_status psp_solve_host(psp_handle h, const double* A_vals_h, int32_t R, const
                               cudaMemcpyHostToDevice, h->stream));
   CUDA_TRY(h, cudaMemcpyAsync(h->stageB_d.p, B_h, sizeof(double) * (size_t)h->n * R,
                               cudaMemcpyHostToDevice, h->stream));
-  if (R == 1 && h->aug_ok) {   // one right-hand side: forward pass fused into the factor
+  if (R == 1) {   // one right-hand side: psp_factor_solve_batch (fused when it pays)
     if ((s = psp_factor_solve_batch(h, (const double*)h->stageA_d.p, (const double*)h->stageB_d.p,
                                     pivot_tol, nullptr)))
       return s;
