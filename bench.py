@@ -371,6 +371,40 @@ def main():
                       "ms_per_step": 1e3 * e2e_s / e2e_steps, "matches_device_result": e2e_ok,
                       "api": "psp_solve_host_async x steps + psp_synchronize (pinned buffers, "
                              "copies back overlapped with the next step), wall clock"}
+        # BASELINE configs[1] as listed (K = 8, one RHS): a latency point, not the
+        # throughput workload; device time per factor_solve + recover
+        try:
+            from psp_inputs import config as _config
+            w1 = _config(1)
+            s1 = w1.system()
+            e1 = w1.eps()
+            sv1 = psp.Solver(local_rank, stream)
+            sv1.psp_symbolic_analyse(s1.n, s1.row_ptr, s1.col_idx, ordering="mindeg")
+            sv1.psp_set_perturbations(e1, s1.d)
+            wp1, wl1, wv1 = psp.ladder_weights_csr(w1.ladders)
+            sv1.psp_set_weights(wp1, wl1, wv1)
+            A1 = torch.tensor(s1.vals, dtype=torch.float64, device="cuda")
+            b1 = torch.tensor(s1.b[:, 0].copy(), dtype=torch.float64, device="cuda")
+            x1 = torch.empty((len(w1.ladders), 1, s1.n), dtype=torch.float64, device="cuda")
+            for _ in range(3):
+                sv1.psp_factor_solve_batch(A1, b1, 0.0)
+                sv1.psp_recover(x1)
+            e0, e9 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for _ in range(20):
+                sv1.psp_factor_solve_batch(A1, b1, 0.0)
+                sv1.psp_recover(x1)
+            e9.record(stream)
+            torch.cuda.synchronize()
+            ms1 = e0.elapsed_time(e9) / 20
+            out["configs1_latency"] = {"workload": w1.name, "K": len(e1), "R": 1,
+                                       "ms_per_step": ms1, "perturbed_solves_per_s": len(e1) / (ms1 * 1e-3),
+                                       "note": "BASELINE configs[1] as listed: one 8-lane slab, "
+                                               "latency-bound (a single warp runs the program)"}
+            sv1.close()
+        except Exception as exc:  # reporting only
+            out["configs1_latency"] = {"error": str(exc)[:200]}
         if not args.no_cpu_baseline:
             cb, Xo, sto, operm = cpu_baseline(s, w, args.cpu_lanes)
             out["cpu_baseline"] = cb
