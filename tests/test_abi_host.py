@@ -105,3 +105,29 @@ def test_host_only_handle_refuses_numeric_calls():
     eps = np.array([1e-3, -1e-3])
     st = psp.lib().psp_set_perturbations(hs.h, 2, psp._np_ptr(eps), psp._np_ptr(np.asarray(s.d)))
     assert st == 8  # PSP_ERR_UNSUPPORTED
+
+
+def test_options_validated_and_reported():
+    """psp_set_option rejects out-of-range values (PSP_ERR_ARG) before any work; the
+    kernel-variant options show up in the symbolic info; PSP_OPT_PHASE_EVENTS needs a
+    device handle (PSP_ERR_STATE on a host-only one)."""
+    hs = psp.HostSymbolic()
+    for name, bad in (("factor_groups", 3), ("factor_lanes", 4), ("factor_slab_warps", 3),
+                      ("factor_pairs", 2), ("factor_tmem", 4), ("solve_tmem", 3), ("growth", 2),
+                      ("phase_events", 2)):
+        with pytest.raises(psp.PSPError) as e:
+            hs.set_option(name, bad)
+        assert e.value.status == 1, name   # PSP_ERR_ARG
+    with pytest.raises(psp.PSPError) as e:
+        hs.set_option("phase_events", 1)
+    assert e.value.status == 3   # PSP_ERR_STATE
+    s = config(1).system()
+    info, _ = hs.analyse(s.n, s.row_ptr, s.col_idx)
+    assert info["factor_pend_smem"] == 2 and info["aug_ok"] == 2     # TMEM variant, fused path
+    hs.set_option("factor_tmem", 2)
+    info, _ = hs.analyse(s.n, s.row_ptr, s.col_idx)
+    assert info["factor_pend_smem"] == 1 and info["factor_warps_per_cta"] == 4
+    hs.set_option("factor_tmem", 1)
+    info3, _ = hs.analyse(s.n, s.row_ptr, s.col_idx)
+    assert info3["factor_pend_smem"] == 2 and info3["aug_max_live"] > info3["max_live"]
+    hs.close()
