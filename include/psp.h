@@ -134,10 +134,15 @@ psp_status psp_destroy(psp_handle h);
  *                         solve kernel launches (for psp_get_phase_times; any time).
  *  PSP_OPT_GROWTH         0 (default); 1: every factorisation also computes the per-lane
  *                         growth factor (psp_get_lane_growth; any time).
+ *  PSP_OPT_COOP           0 (default): automatic — batches of K <= 4 x the SM count use the
+ *                         cooperative kernels (one CTA per system, its factor in shared
+ *                         memory, etree-level steps); 1: always (when the
+ *                         factor fits shared memory); 2: never.  Bitwise-neutral.
  * Errors: ARG (STATE: PSP_OPT_PHASE_EVENTS on a host-only handle). */
 enum { PSP_OPT_FACTOR_GROUPS = 1, PSP_OPT_FACTOR_WARPS = 2, PSP_OPT_FACTOR_LANES = 3,
        PSP_OPT_FACTOR_SLAB_WARPS = 4, PSP_OPT_FACTOR_PAIRS = 5, PSP_OPT_FACTOR_TMEM = 6,
-       PSP_OPT_SOLVE_TMEM = 7, PSP_OPT_PHASE_EVENTS = 8, PSP_OPT_GROWTH = 9 };
+       PSP_OPT_SOLVE_TMEM = 7, PSP_OPT_PHASE_EVENTS = 8, PSP_OPT_GROWTH = 9,
+       PSP_OPT_COOP = 10 };
 psp_status psp_set_option(psp_handle h, int32_t option, int64_t value);
 
 /* Rebind the handle to another stream of the same device. */

@@ -55,6 +55,10 @@ struct psp_ctx {
   // row): used when it needs fewer waves than `launch`'s (PSP_OPT_SOLVE_TMEM = 0)
   psp::LaunchInfo launch_stm;
   bool stm_ok = false;
+  // cooperative small-batch kernels (one CTA per system, level-scheduled)
+  psp::CoopDev coop;
+  bool coop_ok = false;
+  int64_t opt_coop = 0;            // PSP_OPT_COOP: 0 automatic (K <= 4 * SMs), 1 on, 2 off
   // program of the augmented matrix [A | b] (psp_factor_solve_batch); its own slots,
   // stream and factor launch configuration, the rest shared with `plan`
   DevicePlan plan_aug;
@@ -280,6 +284,10 @@ psp_status psp_set_option(psp_handle h, int32_t option, int64_t value) {
       if (value < 0 || value > 2) return fail(h, PSP_ERR_ARG, "PSP_OPT_FACTOR_TMEM must be 0, 1 or 2");
       h->opt_tmem = value;
       return PSP_OK;
+    case PSP_OPT_COOP:
+      if (value < 0 || value > 2) return fail(h, PSP_ERR_ARG, "PSP_OPT_COOP must be 0, 1 or 2");
+      h->opt_coop = value;
+      return PSP_OK;
     case PSP_OPT_GROWTH:
       if (value != 0 && value != 1) return fail(h, PSP_ERR_ARG, "PSP_OPT_GROWTH must be 0 or 1");
       h->growth = value != 0;
@@ -476,6 +484,8 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
   HPa.aug = true;
   psp::build_programs(n, S.lcol, perm, row_ptr_h, col_idx_h, HP);
   psp::build_programs(n, S.lcol, perm, row_ptr_h, col_idx_h, HPa);
+  psp::CoopPlan CP;
+  psp::build_coop(n, S.lcol, perm, row_ptr_h, col_idx_h, HP, CP);
 
   // CSC grouping of A's entries (original numbering) for the deterministic 1-norm
   std::vector<int32_t> acsc_ptr(n + 1, 0), acsc_q(nnzA);
@@ -542,6 +552,20 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
     CUDA_TRY(h, psp::configure_kernels(P, h->launch, (int)h->opt_groups, (int)h->opt_warps,
                                         (int)h->opt_lanes, (int)h->opt_slab_warps, (int)h->opt_tmem,
                           (int)h->opt_solve_tmem));
+  h->coop_ok = false;
+  h->coop = psp::CoopDev{};
+  if (!host_only && psp::coop_smem_bytes(P) <= (size_t)(227 * 1024)) {
+    psp::CoopDev& c = h->coop;
+    c.steps = CP.steps;
+#define UPC(field)                                                    \
+  if ((s = upload(h, CP.field, &c.field))) return s;
+    UPC(birth_src) UPC(birth_diag) UPC(fa_ptr) UPC(fa_l) UPC(fa_d) UPC(fp_ptr) UPC(fp_d) UPC(fp_p)
+    UPC(fb_ptr) UPC(fb_t) UPC(fb_cptr) UPC(fb_l) UPC(fb_u) UPC(ya_ptr) UPC(ya_t) UPC(ya_cptr)
+    UPC(ya_l) UPC(ya_p) UPC(xb_ptr) UPC(xb_r) UPC(xb_d) UPC(xb_cptr) UPC(xb_u) UPC(xb_k)
+#undef UPC
+    CUDA_TRY(h, psp::configure_coop(P));
+    h->coop_ok = true;
+  }
   h->stm_ok = false;
   if (h->opt_solve_tmem == 0) {
     psp::LaunchInfo ls = h->launch;
@@ -663,6 +687,13 @@ static const psp::LaunchInfo& solve_launch(psp_ctx* h, int32_t R = 1) {
   return rounds(h->launch_stm) < rounds(h->launch) ? h->launch_stm : h->launch;
 }
 
+// The cooperative small-batch kernels for this batch? (few systems: one CTA each beats
+// one thread each; PSP_OPT_COOP overrides)
+static bool use_coop(psp_ctx* h) {
+  if (!h->coop_ok || h->opt_coop == 2) return false;
+  return h->opt_coop == 1 || h->K <= 4 * h->n_sm;
+}
+
 // Record the next event of a phase pool on the handle's stream (growing the pool).
 static psp_status phase_mark(psp_ctx* h, std::vector<cudaEvent_t>& pool, size_t& used) {
   if (used == pool.size()) {
@@ -722,10 +753,17 @@ static psp_status factor_impl(psp_handle h, const double* A_vals, double pivot_t
     if ((s = ensure(h, h->growth_d, sizeof(double) * (size_t)h->K_pad))) return s;
     if ((s = ensure(h, h->offmax_d, sizeof(double)))) return s;
   }
-  CUDA_TRY(h, psp::launch_factor(P, LI, P.f_stream, (const double*)h->eps_d.p, tol_dev, pivot_tol,
-                                 (double*)h->V_d.p, (double*)h->fscratch_d.p, (double*)h->fscr_d.p,
-                                 (int32_t*)h->status_d.p, h->K_pad,
-                                 aug ? (double*)h->X_d.p : nullptr, h->stream));
+  if (use_coop(h)) {   // (the augmented program is not needed: the solve does its forward)
+    CUDA_TRY(h, psp::launch_coop_factor(h->plan, h->coop, A_vals, (const double*)h->eps_d.p,
+                                        (const double*)h->dperm_d.p, tol_dev, pivot_tol,
+                                        (double*)h->V_d.p, (int32_t*)h->status_d.p, h->K,
+                                        kBlock / h->launch.f_groups * h->launch.f_lanes, h->stream));
+  } else {
+    CUDA_TRY(h, psp::launch_factor(P, LI, P.f_stream, (const double*)h->eps_d.p, tol_dev, pivot_tol,
+                                   (double*)h->V_d.p, (double*)h->fscratch_d.p, (double*)h->fscr_d.p,
+                                   (int32_t*)h->status_d.p, h->K_pad,
+                                   aug ? (double*)h->X_d.p : nullptr, h->stream));
+  }
   if (h->phase_events) {
     if ((s = phase_mark(h, h->fev, h->nf))) return s;
   }
@@ -765,7 +803,7 @@ psp_status psp_factor_solve_batch(psp_handle h, const double* A_vals, const doub
   if (!h) return PSP_ERR_ARG;
   if (!b) return fail(h, PSP_ERR_ARG, "b required");
   psp_status s;
-  if (h->analysed && !h->aug_fast) {   // the two calls (bitwise the same results)
+  if (h->analysed && (!h->aug_fast || use_coop(h))) {   // the two calls (bitwise the same)
     if ((s = factor_impl(h, A_vals, pivot_tol, lane_status, false, nullptr))) return s;
     return psp_solve_batch(h, 1, b, h->n);
   }
@@ -800,6 +838,17 @@ psp_status psp_solve_batch(psp_handle h, int32_t R, const double* B, int64_t ldb
   if ((s = solve_scratch(h, R))) return s;
   if (h->phase_events) {
     if ((s = phase_mark(h, h->sev, h->ns))) return s;
+  }
+  if (use_coop(h)) {
+    CUDA_TRY(h, psp::launch_coop_solve(h->plan, h->coop, (const double*)h->V_d.p, B, ldb, R,
+                                       (double*)h->X_d.p, h->K,
+                                       kBlock / h->launch.f_groups * h->launch.f_lanes, h->stream));
+    if (h->phase_events) {
+      if ((s = phase_mark(h, h->sev, h->ns))) return s;
+    }
+    h->R = R;
+    h->solved = true;
+    return PSP_OK;
   }
   CUDA_TRY(h, psp::launch_solve(h->plan, solve_launch(h, R), (const double*)h->V_d.p, B, ldb, R,
                                 (double*)h->X_d.p, (double*)h->sscratch_d.p, h->K_pad, true,

@@ -52,6 +52,31 @@ struct DevicePlan {
   const int32_t* acsc_q = nullptr;     // [nnz_A]
 };
 
+// Device copy of the level-scheduled plan of the cooperative small-batch kernels
+// (psp_plan.h CoopPlan): one CTA per system, its factor image in shared memory.
+struct CoopDev {
+  int32_t steps = 0;
+  const int32_t *birth_src = nullptr, *birth_diag = nullptr;
+  const int32_t *fa_ptr = nullptr, *fa_l = nullptr, *fa_d = nullptr;
+  const int32_t *fp_ptr = nullptr, *fp_d = nullptr, *fp_p = nullptr;
+  const int32_t *fb_ptr = nullptr, *fb_t = nullptr, *fb_cptr = nullptr, *fb_l = nullptr, *fb_u = nullptr;
+  const int32_t *ya_ptr = nullptr, *ya_t = nullptr, *ya_cptr = nullptr, *ya_l = nullptr, *ya_p = nullptr;
+  const int32_t *xb_ptr = nullptr, *xb_r = nullptr, *xb_d = nullptr, *xb_cptr = nullptr;
+  const int32_t *xb_u = nullptr, *xb_k = nullptr;
+};
+// Cooperative kernels: factor (births, per step: pivot checks + L columns, then the
+// updates) and solve (forward, backward, R right-hand sides), V and X in the layouts of
+// the batch kernels (LS lanes per factor slab).
+cudaError_t launch_coop_factor(const DevicePlan& p, const CoopDev& c, const double* A,
+                               const double* eps, const double* dperm, const double* tol_dev,
+                               double tol_value, double* V, int32_t* status, int32_t K, int32_t LS,
+                               cudaStream_t stream);
+cudaError_t launch_coop_solve(const DevicePlan& p, const CoopDev& c, const double* V, const double* B,
+                              int64_t ldb, int32_t R, double* X, int32_t K, int32_t LS,
+                              cudaStream_t stream);
+size_t coop_smem_bytes(const DevicePlan& p);
+cudaError_t configure_coop(const DevicePlan& p);
+
 // Launch configuration chosen per plan (host, psp_kernels.cu: choose_launch).
 struct LaunchInfo {
   // factor

@@ -24,6 +24,7 @@
 #include "psp_internal.h"
 
 #include <algorithm>
+#include <array>
 #include <climits>
 #include <cstdint>
 #include <functional>
@@ -203,6 +204,157 @@ void pack_chunks(const std::vector<std::vector<int32_t>>& recs, size_t max_rec,
 }
 
 }  // namespace
+
+void build_coop(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
+                const std::vector<int32_t>& perm, const int32_t* row_ptr_h,
+                const int32_t* col_idx_h, const HostPlan& P, CoopPlan& C) {
+  const int32_t nnzL = P.nnz_L, nnzLU = P.nnz_LU;
+  // etree levels: a pivot's level exceeds its children's (parent = first row of L(:,p))
+  std::vector<int32_t> level(n, 0);
+  int32_t nl = 0;
+  for (int32_t p = 0; p < n; ++p) {
+    if (!lcol[p].empty()) level[lcol[p][0]] = std::max(level[lcol[p][0]], level[p] + 1);
+    nl = std::max(nl, level[p] + 1);
+  }
+  C.steps = nl;
+  auto pos_in = [&](int32_t col, int32_t row) -> int32_t {
+    const auto& v = lcol[col];
+    return (int32_t)(std::lower_bound(v.begin(), v.end(), row) - v.begin());
+  };
+  auto pos = [&](int32_t i, int32_t j) -> int32_t {   // V-image position of entry (i, j)
+    if (i == j) return nnzL + P.dofs[i];
+    if (i > j) return P.lofs[j] + pos_in(j, i);
+    return nnzL + P.dofs[i] + 1 + pos_in(i, j);
+  };
+  auto a_index = [&](int32_t i, int32_t j) -> int32_t {
+    const int32_t r = perm[i], c = perm[j];
+    const int32_t* b = col_idx_h + row_ptr_h[r];
+    const int32_t* e = col_idx_h + row_ptr_h[r + 1];
+    const int32_t* it = std::lower_bound(b, e, c);
+    return (it != e && *it == c) ? (int32_t)(it - col_idx_h) : -1;
+  };
+  C.birth_src.assign(nnzLU, -1);
+  C.birth_diag.assign(nnzLU, -1);
+  for (int32_t p = 0; p < n; ++p) {
+    C.birth_src[pos(p, p)] = a_index(p, p);
+    C.birth_diag[pos(p, p)] = p;
+    for (int32_t i : lcol[p]) {
+      C.birth_src[pos(i, p)] = a_index(i, p);
+      C.birth_src[pos(p, i)] = a_index(p, i);
+    }
+  }
+  // factor A: the L column of every pivot of the step; status over the step's pivots
+  std::vector<std::vector<int32_t>> by_level(nl);
+  for (int32_t p = 0; p < n; ++p) by_level[level[p]].push_back(p);
+  C.fa_ptr.assign(1, 0);
+  C.fp_ptr.assign(1, 0);
+  for (int32_t l = 0; l < nl; ++l) {
+    for (int32_t p : by_level[l]) {
+      C.fp_d.push_back(pos(p, p));
+      C.fp_p.push_back(p);
+      for (size_t k = 0; k < lcol[p].size(); ++k) {
+        C.fa_l.push_back(P.lofs[p] + (int32_t)k);
+        C.fa_d.push_back(pos(p, p));
+      }
+    }
+    C.fa_ptr.push_back((int32_t)C.fa_l.size());
+    C.fp_ptr.push_back((int32_t)C.fp_d.size());
+    C.max_fa = std::max(C.max_fa, C.fa_ptr[l + 1] - C.fa_ptr[l]);
+  }
+  // factor B: contributions per target in ascending pivot order, each at the running
+  // maximum of its contributors' levels
+  {
+    std::vector<std::vector<std::array<int32_t, 3>>> contrib(nnzLU);   // (p, l_pos, u_pos)
+    for (int32_t p = 0; p < n; ++p) {
+      const auto& L = lcol[p];
+      for (size_t a = 0; a < L.size(); ++a)
+        for (size_t b = 0; b < L.size(); ++b)
+          contrib[pos(L[a], L[b])].push_back(
+              {p, P.lofs[p] + (int32_t)a, nnzL + P.dofs[p] + 1 + (int32_t)b});
+    }
+    // step -> list of (target, [contributions])
+    std::vector<std::vector<std::pair<int32_t, std::vector<std::array<int32_t, 3>>>>> st(nl);
+    for (int32_t t = 0; t < nnzLU; ++t) {
+      auto& cl = contrib[t];
+      std::sort(cl.begin(), cl.end());
+      int32_t run = 0, cur = -1;
+      for (const auto& c : cl) {
+        run = std::max(run, level[c[0]]);
+        if (run != cur) {
+          st[run].push_back({t, {}});
+          cur = run;
+        }
+        st[run].back().second.push_back(c);
+      }
+    }
+    C.fb_ptr.assign(1, 0);
+    C.fb_cptr.assign(1, 0);
+    for (int32_t l = 0; l < nl; ++l) {
+      for (const auto& tc : st[l]) {
+        C.fb_t.push_back(tc.first);
+        for (const auto& c : tc.second) {
+          C.fb_l.push_back(c[1]);
+          C.fb_u.push_back(c[2]);
+        }
+        C.fb_cptr.push_back((int32_t)C.fb_l.size());
+      }
+      C.fb_ptr.push_back((int32_t)C.fb_t.size());
+      C.max_fb = std::max(C.max_fb, C.fb_ptr[l + 1] - C.fb_ptr[l]);
+    }
+  }
+  // forward: y_i <- fma(-l_ip, y_p, y_i), p ascending, at running-max steps
+  {
+    std::vector<std::vector<std::array<int32_t, 2>>> contrib(n);   // (p, l_pos)
+    for (int32_t p = 0; p < n; ++p)
+      for (size_t a = 0; a < lcol[p].size(); ++a)
+        contrib[lcol[p][a]].push_back({p, P.lofs[p] + (int32_t)a});
+    std::vector<std::vector<std::pair<int32_t, std::vector<std::array<int32_t, 2>>>>> st(nl);
+    for (int32_t i = 0; i < n; ++i) {
+      auto& cl = contrib[i];
+      std::sort(cl.begin(), cl.end());
+      int32_t run = 0, cur = -1;
+      for (const auto& c : cl) {
+        run = std::max(run, level[c[0]]);
+        if (run != cur) {
+          st[run].push_back({i, {}});
+          cur = run;
+        }
+        st[run].back().second.push_back(c);
+      }
+    }
+    C.ya_ptr.assign(1, 0);
+    C.ya_cptr.assign(1, 0);
+    for (int32_t l = 0; l < nl; ++l) {
+      for (const auto& tc : st[l]) {
+        C.ya_t.push_back(tc.first);
+        for (const auto& c : tc.second) {
+          C.ya_l.push_back(c[1]);
+          C.ya_p.push_back(c[0]);
+        }
+        C.ya_cptr.push_back((int32_t)C.ya_l.size());
+      }
+      C.ya_ptr.push_back((int32_t)C.ya_t.size());
+      C.max_ya = std::max(C.max_ya, C.ya_ptr[l + 1] - C.ya_ptr[l]);
+    }
+  }
+  // backward: levels from the roots down; row p: U(p, :) columns descending
+  C.xb_ptr.assign(1, 0);
+  C.xb_cptr.assign(1, 0);
+  for (int32_t l = nl - 1; l >= 0; --l) {
+    for (int32_t p : by_level[l]) {
+      C.xb_r.push_back(p);
+      C.xb_d.push_back(pos(p, p));
+      const auto& L = lcol[p];
+      for (int32_t k = (int32_t)L.size() - 1; k >= 0; --k) {
+        C.xb_u.push_back(nnzL + P.dofs[p] + 1 + k);
+        C.xb_k.push_back(L[k]);
+      }
+      C.xb_cptr.push_back((int32_t)C.xb_u.size());
+    }
+    C.xb_ptr.push_back((int32_t)C.xb_r.size());
+    C.max_xb = std::max(C.max_xb, C.xb_ptr[C.xb_ptr.size() - 1] - C.xb_ptr[C.xb_ptr.size() - 2]);
+  }
+}
 
 void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
                     const std::vector<int32_t>& perm, const int32_t* row_ptr_h,

@@ -42,6 +42,31 @@ struct HostPlan {
   int32_t s_bwd_chunk = 0;         // first program chunk of the backward records
 };
 
+// Level-scheduled plan of the cooperative small-batch kernels (one CTA per system, the
+// lane's whole factor image in shared memory).  Every list is grouped by step (CSR-style
+// *_ptr over steps); positions index the per-lane factor image (the V layout: L region,
+// then DU region).  A contribution to an entry is scheduled at the running maximum of
+// its contributors' etree levels, in ascending pivot order, so each entry still gets its
+// updates in the canonical order (bitwise the sequential kernels' results).
+struct CoopPlan {
+  int32_t steps = 0;                         // etree height
+  std::vector<int32_t> birth_src;            // [nnz_LU] CSR index of A (permuted entry) or -1
+  std::vector<int32_t> birth_diag;           // [nnz_LU] row p for u_pp entries, else -1
+  // factor step A (per step: pivots of that level): l positions / their pivot's diag
+  std::vector<int32_t> fa_ptr, fa_l, fa_d;   // [steps+1], [.], [.]
+  std::vector<int32_t> fp_ptr, fp_d, fp_p;   // pivots per step: diag position, pivot index
+  // factor step B: per step, targets; per target, its contributions (l_pos, u_pos)
+  std::vector<int32_t> fb_ptr, fb_t, fb_cptr, fb_l, fb_u;
+  // forward: per step, target rows; per target, (l_pos, source row p) ascending p
+  std::vector<int32_t> ya_ptr, ya_t, ya_cptr, ya_l, ya_p;
+  // backward: per step (roots first), rows; per row, (u_pos, column k) descending k
+  std::vector<int32_t> xb_ptr, xb_r, xb_d, xb_cptr, xb_u, xb_k;   // xb_d: u_pp position
+  int32_t max_fa = 0, max_fb = 0, max_ya = 0, max_xb = 0;   // largest step (sizes)
+};
+void build_coop(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
+                const std::vector<int32_t>& perm, const int32_t* row_ptr_h,
+                const int32_t* col_idx_h, const HostPlan& P, CoopPlan& C);
+
 std::vector<int32_t> min_degree_order(int32_t n, const std::vector<std::vector<int32_t>>& adj,
                                       int32_t first);
 EtreeResult symbolic_etree(int32_t n, const std::vector<std::vector<int32_t>>& adjp);

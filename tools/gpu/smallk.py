@@ -14,9 +14,9 @@ A = torch.tensor(s.vals, dtype=torch.float64, device="cuda")
 B = torch.tensor(s.b.T.copy(), dtype=torch.float64, device="cuda")
 ref = None
 for gjpt in sys.argv[1].split(","):
-    G, J, P, T = (int(x) for x in (gjpt + ":0:0:0").split(":")[:4])
+    G, J, P, T, C = (int(x) for x in (gjpt + ":0:0:0:0").split(":")[:5])
     sv = psp.Solver(0)
-    for k, v in (("factor_groups", G), ("factor_lanes", J), ("factor_slab_warps", P), ("factor_tmem", T),
+    for k, v in (("factor_groups", G), ("factor_lanes", J), ("factor_slab_warps", P), ("factor_tmem", T), ("coop", C),
                  ("phase_events", 1)):
         sv.psp_set_option(k, v)
     sv.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, "mindeg")
