@@ -487,6 +487,46 @@ def test_degenerate_patterns_fused_and_separate(n):
     assert np.array_equal(outs[0], Xo) and np.array_equal(outs[1], Xo)
 
 
+@pytest.mark.parametrize("ci,order,K", [(0, "mindeg", 37), (1, "mindeg", 8), (1, "mindeg_first", 40),
+                                        (2, "mindeg", 64)])
+def test_coop_kernels_bitwise_vs_batch_kernels(ci, order, K):
+    """PSP_OPT_COOP: the cooperative small-batch kernels (one CTA per system, etree-level
+    steps) against the batch kernels and the oracle: factor entries, statuses and
+    solutions bitwise (slack-slot and leading-zero orderings, multi-RHS on cfg2, a
+    failing lane: eps = 0 in the leading-zero regime)."""
+    s = config(ci).system()
+    rng = np.random.default_rng(K + ci)
+    eps = rng.choice([-1, 1], K) * 10.0 ** rng.uniform(-6, -2, K)
+    first = s.slot_p if order == "mindeg_first" else -1
+    if order == "mindeg_first":
+        eps[3] = 0.0   # unperturbed: the structural zero pivot fails this lane
+    A = torch.tensor(s.vals, dtype=torch.float64, device="cuda")
+    B = torch.tensor(s.b.T.copy(), dtype=torch.float64, device="cuda")
+    outs = []
+    for coop in (1, 2):
+        solver = psp.Solver(0)
+        solver.psp_set_option("coop", coop)
+        solver.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering=order, first_node=first)
+        info, perm = solver.psp_get_symbolic_info()
+        solver.psp_set_perturbations(eps, s.d)
+        solver.psp_factor_batch(A, 0.0)
+        solver.psp_solve_batch(B)
+        rc, st = solver.psp_get_lane_status()
+        F = [solver.psp_get_factor(k, info["nnz_LU"]) for k in sorted({0, K // 2, K - 1})]
+        outs.append((solver.psp_get_solutions().cpu().numpy(), st, F, perm))
+    (X1, st1, F1, perm), (X2, st2, F2, _) = outs
+    assert np.array_equal(st1, st2)
+    assert all(np.array_equal(a, b, equal_nan=True) for a, b in zip(F1, F2))
+    assert np.array_equal(X1, X2, equal_nan=True)
+    tol = oracle.default_tol(s.n, s.row_ptr, s.col_idx, s.vals)
+    Xo, sto = oracle.SparseOracle(s, perm).batch(eps, tol)
+    ok = sto == 0
+    assert np.array_equal(st1 != 0, sto != 0)
+    assert np.array_equal(X1[ok], Xo[ok])
+    if order == "mindeg_first":
+        assert st1[3] != 0
+
+
 def test_sharded_recover_partials_sum_to_full():
     """Row a6 on one GPU: lanes split over two handles (a ladder straddles the split);
     each recovers its partial sums with its shard of the weights; their sum equals the
