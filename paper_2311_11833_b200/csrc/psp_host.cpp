@@ -554,17 +554,65 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
                           (int)h->opt_solve_tmem));
   h->coop_ok = false;
   h->coop = psp::CoopDev{};
-  if (!host_only && psp::coop_smem_bytes(P) <= (size_t)(227 * 1024)) {
+  if (!host_only) {
+    // packed plans (16-bit fields): positions, rows and contribution counts must fit
+    const size_t nc = std::max({CP.fb_l.size(), CP.ya_l.size(), CP.xb_u.size()});
+    bool fits = P.nnz_LU < 65536 && n < 65536 && nc < 65536;
+    std::vector<uint32_t> fw, sw;
     psp::CoopDev& c = h->coop;
-    c.steps = CP.steps;
-#define UPC(field)                                                    \
-  if ((s = upload(h, CP.field, &c.field))) return s;
-    UPC(birth_src) UPC(birth_diag) UPC(fa_ptr) UPC(fa_l) UPC(fa_d) UPC(fp_ptr) UPC(fp_d) UPC(fp_p)
-    UPC(fb_ptr) UPC(fb_t) UPC(fb_cptr) UPC(fb_l) UPC(fb_u) UPC(ya_ptr) UPC(ya_t) UPC(ya_cptr)
-    UPC(ya_l) UPC(ya_p) UPC(xb_ptr) UPC(xb_r) UPC(xb_d) UPC(xb_cptr) UPC(xb_u) UPC(xb_k)
-#undef UPC
-    CUDA_TRY(h, psp::configure_coop(P));
-    h->coop_ok = true;
+    if (fits) {
+      const int32_t S1 = CP.steps + 1;
+      auto add_ptr = [](std::vector<uint32_t>& w, const std::vector<int32_t>& ptr) {
+        for (int32_t x : ptr) w.push_back((uint32_t)x);
+      };
+      auto pack = [](std::vector<uint32_t>& w, const std::vector<int32_t>& lo, const std::vector<int32_t>& hi) {
+        for (size_t q = 0; q < lo.size(); ++q) w.push_back((uint32_t)lo[q] | ((uint32_t)hi[q] << 16));
+      };
+      auto pad4 = [](std::vector<uint32_t>& w) { while (w.size() % 4) w.push_back(0); };
+      add_ptr(fw, CP.fa_ptr); add_ptr(fw, CP.fp_ptr); add_ptr(fw, CP.fb_ptr);
+      pad4(fw); c.fo_fa = (int32_t)fw.size(); pack(fw, CP.fa_l, CP.fa_d);
+      pad4(fw); c.fo_fp = (int32_t)fw.size(); pack(fw, CP.fp_d, CP.fp_p);
+      pad4(fw); c.fo_fbt = (int32_t)fw.size();
+      {
+        std::vector<int32_t> start(CP.fb_cptr.begin(), CP.fb_cptr.end() - 1);
+        pack(fw, CP.fb_t, start);
+        fw.push_back((uint32_t)CP.fb_cptr.back() << 16);   // sentinel: end of the last target
+      }
+      pad4(fw); c.fo_fbc = (int32_t)fw.size(); pack(fw, CP.fb_l, CP.fb_u);
+      pad4(fw); c.f_words = (int32_t)fw.size();
+      add_ptr(sw, CP.ya_ptr); add_ptr(sw, CP.xb_ptr);
+      pad4(sw); c.so_yat = (int32_t)sw.size();
+      {
+        std::vector<int32_t> start(CP.ya_cptr.begin(), CP.ya_cptr.end() - 1);
+        pack(sw, CP.ya_t, start);
+        sw.push_back((uint32_t)CP.ya_cptr.back() << 16);
+      }
+      pad4(sw); c.so_yac = (int32_t)sw.size(); pack(sw, CP.ya_l, CP.ya_p);
+      pad4(sw); c.so_xbr = (int32_t)sw.size();
+      {
+        std::vector<int32_t> start(CP.xb_cptr.begin(), CP.xb_cptr.end() - 1);
+        pack(sw, CP.xb_r, start);
+        sw.push_back((uint32_t)CP.xb_cptr.back() << 16);
+      }
+      pad4(sw); c.so_xbd = (int32_t)sw.size();
+      for (int32_t d : CP.xb_d) sw.push_back((uint32_t)d);
+      pad4(sw); c.so_xbc = (int32_t)sw.size(); pack(sw, CP.xb_u, CP.xb_k);
+      pad4(sw); c.s_words = (int32_t)sw.size();
+      (void)S1;
+      c.steps = CP.steps;
+      fits = psp::coop_smem_bytes(P, c, false) <= (size_t)(227 * 1024) &&
+             psp::coop_smem_bytes(P, c, true) <= (size_t)(227 * 1024);
+    }
+    if (fits) {
+      if ((s = upload(h, CP.birth_src, &c.birth_src))) return s;
+      if ((s = upload(h, CP.birth_diag, &c.birth_diag))) return s;
+      if ((s = upload(h, fw, &c.fplan))) return s;
+      if ((s = upload(h, sw, &c.splan))) return s;
+      CUDA_TRY(h, psp::configure_coop(P, c));
+      h->coop_ok = true;
+    } else {
+      c = psp::CoopDev{};
+    }
   }
   h->stm_ok = false;
   if (h->opt_solve_tmem == 0) {
@@ -689,9 +737,11 @@ static const psp::LaunchInfo& solve_launch(psp_ctx* h, int32_t R = 1) {
 
 // The cooperative small-batch kernels for this batch? (few systems: one CTA each beats
 // one thread each; PSP_OPT_COOP overrides)
-static bool use_coop(psp_ctx* h) {
+static bool use_coop(psp_ctx* h, int32_t R = 1) {
   if (!h->coop_ok || h->opt_coop == 2) return false;
-  return h->opt_coop == 1 || h->K <= 4 * h->n_sm;
+  // (solves: a CTA runs its right-hand sides in turn; from ~12 of them the batch
+  // solve's warp-per-(block, RHS) parallelism wins: measured on cfg2, R = 16)
+  return h->opt_coop == 1 || (h->K <= 4 * h->n_sm && R <= 8);
 }
 
 // Record the next event of a phase pool on the handle's stream (growing the pool).
@@ -839,7 +889,7 @@ psp_status psp_solve_batch(psp_handle h, int32_t R, const double* B, int64_t ldb
   if (h->phase_events) {
     if ((s = phase_mark(h, h->sev, h->ns))) return s;
   }
-  if (use_coop(h)) {
+  if (use_coop(h, R)) {
     CUDA_TRY(h, psp::launch_coop_solve(h->plan, h->coop, (const double*)h->V_d.p, B, ldb, R,
                                        (double*)h->X_d.p, h->K,
                                        kBlock / h->launch.f_groups * h->launch.f_lanes, h->stream));

@@ -57,12 +57,14 @@ struct DevicePlan {
 struct CoopDev {
   int32_t steps = 0;
   const int32_t *birth_src = nullptr, *birth_diag = nullptr;
-  const int32_t *fa_ptr = nullptr, *fa_l = nullptr, *fa_d = nullptr;
-  const int32_t *fp_ptr = nullptr, *fp_d = nullptr, *fp_p = nullptr;
-  const int32_t *fb_ptr = nullptr, *fb_t = nullptr, *fb_cptr = nullptr, *fb_l = nullptr, *fb_u = nullptr;
-  const int32_t *ya_ptr = nullptr, *ya_t = nullptr, *ya_cptr = nullptr, *ya_l = nullptr, *ya_p = nullptr;
-  const int32_t *xb_ptr = nullptr, *xb_r = nullptr, *xb_d = nullptr, *xb_cptr = nullptr;
-  const int32_t *xb_u = nullptr, *xb_k = nullptr;
+  // packed plans (uint32 words, 16-bit fields), copied into shared memory by each CTA:
+  // factor: [fa_ptr, fp_ptr, fb_ptr][steps+1] | fa (l | d<<16) | fp (d | p<<16) |
+  //         fbt (t | start<<16, + sentinel) | fbc (l | u<<16)
+  // solve:  [ya_ptr, xb_ptr][steps+1] | yat (i | start<<16, + sentinel) | yac (l | p<<16) |
+  //         xbr (r | start<<16, + sentinel) | xbd (u_pp position) | xbc (u | k<<16)
+  const uint32_t *fplan = nullptr, *splan = nullptr;
+  int32_t f_words = 0, fo_fa = 0, fo_fp = 0, fo_fbt = 0, fo_fbc = 0;
+  int32_t s_words = 0, so_yat = 0, so_yac = 0, so_xbr = 0, so_xbd = 0, so_xbc = 0;
 };
 // Cooperative kernels: factor (births, per step: pivot checks + L columns, then the
 // updates) and solve (forward, backward, R right-hand sides), V and X in the layouts of
@@ -74,8 +76,8 @@ cudaError_t launch_coop_factor(const DevicePlan& p, const CoopDev& c, const doub
 cudaError_t launch_coop_solve(const DevicePlan& p, const CoopDev& c, const double* V, const double* B,
                               int64_t ldb, int32_t R, double* X, int32_t K, int32_t LS,
                               cudaStream_t stream);
-size_t coop_smem_bytes(const DevicePlan& p);
-cudaError_t configure_coop(const DevicePlan& p);
+size_t coop_smem_bytes(const DevicePlan& p, const CoopDev& c, bool solve);
+cudaError_t configure_coop(const DevicePlan& p, const CoopDev& c);
 
 // Launch configuration chosen per plan (host, psp_kernels.cu: choose_launch).
 struct LaunchInfo {
