@@ -400,8 +400,8 @@ def main():
             ms1 = e0.elapsed_time(e9) / 20
             out["configs1_latency"] = {"workload": w1.name, "K": len(e1), "R": 1,
                                        "ms_per_step": ms1, "perturbed_solves_per_s": len(e1) / (ms1 * 1e-3),
-                                       "note": "BASELINE configs[1] as listed: one 8-lane slab, "
-                                               "latency-bound (a single warp runs the program)"}
+                                       "note": "BASELINE configs[1] as listed: 8 systems, latency-bound; "
+                                               "cooperative kernels (a CTA per system, level-scheduled)"}
             sv1.close()
         except Exception as exc:  # reporting only
             out["configs1_latency"] = {"error": str(exc)[:200]}
