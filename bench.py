@@ -192,6 +192,8 @@ def main():
     ap.add_argument("--cpu-lanes", type=int, default=512, help="oracle sample for cpu_baseline")
     ap.add_argument("--ref-lanes", type=int, default=256, help="oracle lanes per reference step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-latency-point", action="store_true",
+                    help="skip the configs[1] (K = 8) latency point (profiling runs)")
     ap.add_argument("--groups", type=int, default=0, help="PSP_OPT_FACTOR_GROUPS (0 = auto)")
     ap.add_argument("--warps", type=int, default=0, help="PSP_OPT_FACTOR_WARPS (0 = auto)")
     ap.add_argument("--separate", action="store_true",
@@ -374,6 +376,8 @@ def main():
         # BASELINE configs[1] as listed (K = 8, one RHS): a latency point, not the
         # throughput workload; device time per factor_solve + recover
         try:
+            if args.no_latency_point:
+                raise RuntimeError("skipped (--no-latency-point)")
             from psp_inputs import config as _config
             w1 = _config(1)
             s1 = w1.system()
