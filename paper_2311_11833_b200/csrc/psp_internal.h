@@ -103,6 +103,8 @@ struct LaunchInfo {
   int s_ctas_per_sm = 0;
   bool s_tmem = false;         // live slots in tensor memory (solve_kernel_tmem)
   int s_yrows = 16;            // rows per stage of the solve's y ring
+  int n_sm = 148;              // SMs of the device (a batch smaller than one round is
+                               // spread over all of them with fewer warps per CTA)
   int s_tmem_cols = 0;         // TMEM columns allocated per CTA
 };
 
