@@ -134,7 +134,7 @@ psp_status psp_destroy(psp_handle h);
  *                         solve kernel launches (for psp_get_phase_times; any time).
  *  PSP_OPT_GROWTH         0 (default); 1: every factorisation also computes the per-lane
  *                         growth factor (psp_get_lane_growth; any time).
- *  PSP_OPT_COOP           0 (default): automatic — batches of K <= 4 x the SM count use the
+ *  PSP_OPT_COOP           0 (default): automatic — batches of K <= 8 x the SM count use the
  *                         cooperative kernels (one CTA per system, its factor in shared
  *                         memory, etree-level steps); 1: always (when the
  *                         factor fits shared memory); 2: never.  Bitwise-neutral.

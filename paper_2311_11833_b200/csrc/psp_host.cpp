@@ -741,7 +741,7 @@ static bool use_coop(psp_ctx* h, int32_t R = 1) {
   if (!h->coop_ok || h->opt_coop == 2) return false;
   // (solves: a CTA runs its right-hand sides in turn; from ~12 of them the batch
   // solve's warp-per-(block, RHS) parallelism wins: measured on cfg2, R = 16)
-  return h->opt_coop == 1 || (h->K <= 4 * h->n_sm && R <= 8);
+  return h->opt_coop == 1 || (h->K <= 8 * h->n_sm && R <= 8);
 }
 
 // Record the next event of a phase pool on the handle's stream (growing the pool).
