@@ -58,7 +58,7 @@ struct psp_ctx {
   // cooperative small-batch kernels (one CTA per system, level-scheduled)
   psp::CoopDev coop;
   bool coop_ok = false;
-  int64_t opt_coop = 0;            // PSP_OPT_COOP: 0 automatic (K <= 4 * SMs), 1 on, 2 off
+  int64_t opt_coop = 0;            // PSP_OPT_COOP: 0 automatic (K <= 8 * SMs), 1 on, 2 off
   // program of the augmented matrix [A | b] (psp_factor_solve_batch); its own slots,
   // stream and factor launch configuration, the rest shared with `plan`
   DevicePlan plan_aug;
