@@ -527,6 +527,25 @@ def test_coop_kernels_bitwise_vs_batch_kernels(ci, order, K):
         assert st1[3] != 0
 
 
+def test_phase_times_cover_the_launches():
+    """PSP_OPT_PHASE_EVENTS / psp_get_phase_times: mean device time of the factor and the
+    solve launches since the last read (positive, and reset by the read)."""
+    s = config(1).system()
+    eps = np.tile([1e-3, -1e-3], 64)
+    solver = psp.Solver(0)
+    solver.psp_set_option("phase_events", 1)
+    solver.psp_set_option("coop", 2)
+    solver.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering="mindeg")
+    solver.psp_set_perturbations(eps, s.d)
+    A = torch.tensor(s.vals, dtype=torch.float64, device="cuda")
+    b = torch.tensor(s.b[:, 0].copy(), dtype=torch.float64, device="cuda")
+    for _ in range(3):
+        solver.psp_factor_solve_batch(A, b, 0.0)
+    tf, ts = solver.psp_get_phase_times()
+    assert tf > 0 and ts > 0
+    assert solver.psp_get_phase_times() == (0.0, 0.0)
+
+
 def test_sharded_recover_partials_sum_to_full():
     """Row a6 on one GPU: lanes split over two handles (a ladder straddles the split);
     each recovers its partial sums with its shard of the weights; their sum equals the
