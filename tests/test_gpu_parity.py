@@ -546,6 +546,62 @@ def test_phase_times_cover_the_launches():
     assert solver.psp_get_phase_times() == (0.0, 0.0)
 
 
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_random_patterns_all_paths(seed):
+    """Random structurally symmetric patterns with a few dense rows/columns (pivots with
+    c > kFusedMax: scratch rows and UPDATE records; supernode pairs; zero diagonals),
+    random K: the batch kernels (plain and fused) and the cooperative kernels, all
+    bitwise against the oracle."""
+    rng = np.random.default_rng(100 + seed)
+    n = int(rng.integers(40, 90))
+    M = (rng.random((n, n)) < 0.05).astype(float)
+    for hub in rng.choice(n, 3, replace=False):   # dense hubs -> large fronts
+        M[hub, :] = M[:, hub] = (rng.random(n) < 0.6)
+    M = np.maximum(M, M.T)
+    np.fill_diagonal(M, rng.random(n) < 0.8)      # some structurally zero diagonals
+    vals = rng.normal(size=(n, n)) * M
+    vals += np.diag(np.where(np.diag(M) > 0, 4.0 * np.sign(rng.normal(size=n)), 0.0))
+
+    class _S:
+        pass
+    s = _S()
+    rp, ci, v = [0], [], []
+    for i in range(n):
+        for j in range(n):
+            if M[i, j] != 0 or i == j:
+                ci.append(j)
+                v.append(vals[i, j])
+        rp.append(len(ci))
+    s.n, s.row_ptr, s.col_idx, s.vals = n, np.array(rp, np.int32), np.array(ci, np.int32), np.array(v)
+    s.d = rng.normal(size=n)
+    s.d /= np.max(np.abs(s.d))
+    s.b = rng.normal(size=(n, 1))
+    K = int(rng.integers(5, 150))
+    eps = rng.choice([-1, 1], K) * 10.0 ** rng.uniform(-4, -1, K)
+    A = torch.tensor(s.vals, dtype=torch.float64, device="cuda")
+    b = torch.tensor(s.b[:, 0].copy(), dtype=torch.float64, device="cuda")
+    res = []
+    for coop, fused in ((2, False), (2, True), (1, False)):
+        solver = psp.Solver(0)
+        solver.psp_set_option("coop", coop)
+        solver.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering="mindeg")
+        info, perm = solver.psp_get_symbolic_info()
+        solver.psp_set_perturbations(eps, s.d)
+        if fused:
+            solver.psp_factor_solve_batch(A, b, 1e-300)
+        else:
+            solver.psp_factor_batch(A, 1e-300)
+            solver.psp_solve_batch(b.view(1, -1))
+        rc, st = solver.psp_get_lane_status()
+        res.append((solver.psp_get_solutions().cpu().numpy(), st, info))
+    Xo, sto = oracle.SparseOracle(s, perm).batch(eps, 1e-300)
+    ok = sto == 0
+    for X, st, info in res:
+        assert np.array_equal(st != 0, sto != 0)
+        assert np.array_equal(X[ok], Xo[ok])
+    assert res[0][2]["max_live"] > 0
+
+
 def test_sharded_recover_partials_sum_to_full():
     """Row a6 on one GPU: lanes split over two handles (a ladder straddles the split);
     each recovers its partial sums with its shard of the weights; their sum equals the
