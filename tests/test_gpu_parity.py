@@ -546,7 +546,7 @@ def test_phase_times_cover_the_launches():
     assert solver.psp_get_phase_times() == (0.0, 0.0)
 
 
-@pytest.mark.parametrize("seed", [1, 2, 3])
+@pytest.mark.parametrize("seed", [1, 2, 3, 1009])
 def test_random_patterns_all_paths(seed):
     """Random structurally symmetric patterns with a few dense rows/columns (pivots with
     c > kFusedMax: scratch rows and UPDATE records; supernode pairs; zero diagonals),

@@ -20,6 +20,7 @@ for K in [int(k) for k in (sys.argv[1] if len(sys.argv) > 1 else "33,1000,8192,6
         sv.psp_set_option("solve_tmem", int(os.environ.get("PSP_STM", "0")))
         sv.psp_set_option("factor_warps", int(os.environ.get("PSP_FW", "0")))
         sv.psp_set_option("factor_tmem", int(os.environ.get("PSP_FT", "0")))
+        sv.psp_set_option("coop", int(os.environ.get("PSP_COOP", "0")))
         sv.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, "mindeg")
         info, perm = sv.psp_get_symbolic_info()
         sv.psp_set_perturbations(eps, s.d)
