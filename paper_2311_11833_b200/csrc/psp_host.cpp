@@ -644,7 +644,10 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
   h->launch_aug = la;
   {
     auto store = [](const psp::LaunchInfo& li) { return li.f_tmem ? 2 : (li.f_pend_smem ? 1 : 0); };
-    h->aug_fast = h->aug_ok && store(la) == store(h->launch);
+    // (fused only with the TMEM store: the shared-memory-only augmented kernel gave wrong
+    // factors for one-warp CTAs with ~220 KB of slots in the random-pattern stress —
+    // DESIGN.md §10a; those programs run factor + solve, bitwise the same results)
+    h->aug_fast = h->aug_ok && store(la) == store(h->launch) && la.f_tmem;
   }
   h->plan = P;
   h->perm = perm;

@@ -546,16 +546,16 @@ def test_phase_times_cover_the_launches():
     assert solver.psp_get_phase_times() == (0.0, 0.0)
 
 
-@pytest.mark.parametrize("seed", [1, 2, 3, 1009])
-def test_random_patterns_all_paths(seed):
+@pytest.mark.parametrize("seed", [1, 2, 3, 1009, 5120, 5141])
+def test_random_patterns_all_paths(seed, hubs=3, density=0.05):
     """Random structurally symmetric patterns with a few dense rows/columns (pivots with
     c > kFusedMax: scratch rows and UPDATE records; supernode pairs; zero diagonals),
     random K: the batch kernels (plain and fused) and the cooperative kernels, all
     bitwise against the oracle."""
     rng = np.random.default_rng(100 + seed)
     n = int(rng.integers(40, 90))
-    M = (rng.random((n, n)) < 0.05).astype(float)
-    for hub in rng.choice(n, 3, replace=False):   # dense hubs -> large fronts
+    M = (rng.random((n, n)) < density).astype(float)
+    for hub in rng.choice(n, hubs, replace=False):   # dense hubs -> large fronts
         M[hub, :] = M[:, hub] = (rng.random(n) < 0.6)
     M = np.maximum(M, M.T)
     np.fill_diagonal(M, rng.random(n) < 0.8)      # some structurally zero diagonals
@@ -600,6 +600,13 @@ def test_random_patterns_all_paths(seed):
         assert np.array_equal(st != 0, sto != 0)
         assert np.array_equal(X[ok], Xo[ok])
     assert res[0][2]["max_live"] > 0
+
+
+@pytest.mark.parametrize("seed", [7001, 7002, 7003])
+def test_random_sparse_patterns_tmem_fused(seed):
+    """Random sparse patterns whose slots fit TMEM (the fused augmented program runs on
+    the TMEM factor kernel): all paths bitwise against the oracle."""
+    test_random_patterns_all_paths(seed, hubs=0, density=0.035)
 
 
 def test_sharded_recover_partials_sum_to_full():

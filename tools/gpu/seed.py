@@ -84,3 +84,6 @@ print("F fused lane0[:6]", Ff[0][:6])
 print("fused X lane0[:4]", res["fused"][0][0][0][:4], "oracle", Xo[0][0][:4])
 torch.cuda.synchronize()
 print("cuda ok")
+print("L[0:8] batch", Fb[0][:8])
+print("L[0:8] fused", Ff[0][:8])
+print("lane1 batch", Fb[1][:4], "fused", Ff[1][:4])
