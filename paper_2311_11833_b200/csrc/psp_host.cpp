@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <set>
 #include <string>
@@ -632,8 +633,11 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
   Pa.c_scr = HP.c_max + 1 > psp::kFusedMax ? HP.c_max + 1 : 0;
   Pa.f_npatch = (int32_t)HPa.f_patch_pos.size();
   psp::LaunchInfo la = h->launch;
-  // (the augmented factor kernels exist for G = J = P = 1 only)
-  h->aug_ok = (h->opt_groups <= 1 && h->opt_lanes <= 1 && h->opt_slab_warps <= 1) &&
+  // (the augmented factor kernels exist for G = J = P = 1 only, and the factor they write
+  // must have the plain launch's lane layout — V[slab][item][LS], LS = 32 / G * J — that
+  // the solve, psp_get_factor and the growth pass read: only when the plain launch is
+  // (1, 1, 1) too)
+  h->aug_ok = h->launch.f_groups == 1 && h->launch.f_lanes == 1 && h->launch.f_slab_warps == 1 &&
               psp::choose_launch(Pa, la, 1, (int)h->opt_warps, 1, 1, (int)h->opt_tmem, 2);
   if (h->aug_ok && !host_only) {   // (its stream is patched in place, like plan's)
     if ((s = upload(h, HPa.f_stream, &Pa.f_stream))) return s;
@@ -644,10 +648,7 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
   h->launch_aug = la;
   {
     auto store = [](const psp::LaunchInfo& li) { return li.f_tmem ? 2 : (li.f_pend_smem ? 1 : 0); };
-    // (fused only with the TMEM store: the shared-memory-only augmented kernel gave wrong
-    // factors for one-warp CTAs with ~220 KB of slots in the random-pattern stress —
-    // DESIGN.md §10a; those programs run factor + solve, bitwise the same results)
-    h->aug_fast = h->aug_ok && store(la) == store(h->launch) && la.f_tmem;
+    h->aug_fast = h->aug_ok && store(la) == store(h->launch);
   }
   h->plan = P;
   h->perm = perm;
