@@ -601,16 +601,21 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
       pad4(sw); c.s_words = (int32_t)sw.size();
       (void)S1;
       c.steps = CP.steps;
-      fits = psp::coop_smem_bytes(P, c, false) <= (size_t)(227 * 1024) &&
-             psp::coop_smem_bytes(P, c, true) <= (size_t)(227 * 1024);
+      // (the kernels' static shared memory, a few words, counts against the same 227 KB)
+      fits = psp::coop_smem_bytes(P, c, false) <= (size_t)(227 * 1024 - 256) &&
+             psp::coop_smem_bytes(P, c, true) <= (size_t)(227 * 1024 - 256);
     }
     if (fits) {
       if ((s = upload(h, CP.birth_src, &c.birth_src))) return s;
       if ((s = upload(h, CP.birth_diag, &c.birth_diag))) return s;
       if ((s = upload(h, fw, &c.fplan))) return s;
       if ((s = upload(h, sw, &c.splan))) return s;
-      CUDA_TRY(h, psp::configure_coop(P, c));
-      h->coop_ok = true;
+      if (psp::configure_coop(P, c) == cudaSuccess) {
+        h->coop_ok = true;
+      } else {   // (an unusable configuration only disables the cooperative path)
+        cudaGetLastError();
+        c = psp::CoopDev{};
+      }
     } else {
       c = psp::CoopDev{};
     }

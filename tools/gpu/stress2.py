@@ -45,6 +45,9 @@ for t in range(N):
     s.b = rng.normal(size=(s.n, R))
     K = int(rng.integers(1, 300))
     eps = rng.choice([-1, 1], K) * 10.0 ** rng.uniform(-4, -1, K)
+    if rng.random() < 0.3:
+        eps[rng.random(K) < 0.1] = 0.0   # unperturbed lanes: zero diagonals fail them
+    tol = 0.0 if rng.random() < 0.5 else 1e-300
     order = str(rng.choice(["mindeg", "natural"]))
     G = int(rng.choice([0, 0, 1, 2, 4]))
     J = int(rng.choice([0, 1, 2])) if G in (2, 4) else 0
@@ -61,9 +64,9 @@ for t in range(N):
         A = torch.tensor(s.vals, dtype=torch.float64, device="cuda")
         B = torch.tensor(s.b.T.copy(), dtype=torch.float64, device="cuda")
         if fused:
-            sv.psp_factor_solve_batch(A, B[0].contiguous(), 1e-300)
+            sv.psp_factor_solve_batch(A, B[0].contiguous(), tol)
         else:
-            sv.psp_factor_batch(A, 1e-300)
+            sv.psp_factor_batch(A, tol)
             sv.psp_solve_batch(B)
         rc, st = sv.psp_get_lane_status()
         X = sv.psp_get_solutions().cpu().numpy()
@@ -71,7 +74,8 @@ for t in range(N):
     except psp.PSPError as e:
         print(t, "config refused:", str(e)[:100], flush=True)
         continue
-    Xo, sto = oracle.SparseOracle(s, perm).batch(eps, 1e-300)
+    otol = oracle.default_tol(s.n, s.row_ptr, s.col_idx, s.vals) if tol == 0.0 else tol
+    Xo, sto = oracle.SparseOracle(s, perm).batch(eps, otol)
     ok = sto == 0
     good = np.array_equal(st != 0, sto != 0) and np.array_equal(X[ok], Xo[ok])
     if not good:
