@@ -68,6 +68,22 @@ for t in range(N):
         else:
             sv.psp_factor_batch(A, tol)
             sv.psp_solve_batch(B)
+        # random weights: ladder-like contiguous runs or arbitrary lane subsets
+        Wn = int(rng.integers(1, 6))
+        Wm = np.zeros((Wn, K))
+        for w in range(Wn):
+            if rng.random() < 0.5:
+                k0 = int(rng.integers(0, K)); ln = int(rng.integers(1, 9))
+                Wm[w, k0:k0 + ln] = rng.normal(size=len(range(k0, min(K, k0 + ln))))
+            else:
+                Wm[w, rng.random(K) < 0.2] = 1.0
+                Wm[w] *= rng.normal(size=K)
+        ptr, lane, val = [0], [], []
+        for w in range(Wn):
+            nz = np.nonzero(Wm[w])[0]
+            lane += list(nz); val += list(Wm[w, nz]); ptr.append(len(lane))
+        sv.psp_set_weights(np.array(ptr, np.int32), np.array(lane, np.int32), np.array(val))
+        xh = sv.psp_recover().cpu().numpy()
         rc, st = sv.psp_get_lane_status()
         X = sv.psp_get_solutions().cpu().numpy()
         sv.close()
@@ -78,6 +94,10 @@ for t in range(N):
     Xo, sto = oracle.SparseOracle(s, perm).batch(eps, otol)
     ok = sto == 0
     good = np.array_equal(st != 0, sto != 0) and np.array_equal(X[ok], Xo[ok])
+    rows_ok = [w for w in range(Wn) if np.all(ok[np.nonzero(Wm[w])[0]])]
+    if rows_ok:
+        xo = oracle.combine(Wm[rows_ok], np.nan_to_num(Xo))
+        good = good and np.array_equal(xh[rows_ok], xo)
     if not good:
         bad += 1
         print(t, f"FAILED n={s.n} K={K} R={R} order={order} G={G} J={J} T={T} C={C} fused={fused} "
