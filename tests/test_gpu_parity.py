@@ -6,6 +6,8 @@ Bar (BASELINE north_star): per-lane solutions within 1e-11 relati
 equal; recovered x within 1e-10 relative of the oracle's recovered x; statuses
 (integers) bit-exact.  Sizes: the oracle runs every lane where it finishes in
 seconds (configs 0-1, ragged K), sampled lanes at the full BASELINE sizes."""
+import os
+
 import numpy as np
 import pytest
 
@@ -17,6 +19,8 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 from paper_2311_11833_b200 import psp  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def gpu_run(s, eps, ordering_kind="mindeg", first=-1, tol=0.0, B=None, ladders=None,
@@ -607,6 +611,19 @@ def test_random_sparse_patterns_tmem_fused(seed):
     """Random sparse patterns whose slots fit TMEM (the fused augmented program runs on
     the TMEM factor kernel): all paths bitwise against the oracle."""
     test_random_patterns_all_paths(seed, hubs=0, density=0.035)
+
+
+def test_random_configurations_stress():
+    """30 random configurations of tools/gpu/stress2.py (patterns with hubs and zero
+    diagonals, orderings, R, forced G/J, TMEM, coop, fused, failing lanes, default
+    tolerance, random weight rows): solutions, statuses and recovered rows bitwise
+    against the oracle."""
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "gpu", "stress2.py"), "30"],
+                       capture_output=True, text=True, cwd=ROOT, env={**os.environ, "PSP_SEED0": "123000"})
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "failures 0 of 30" in r.stdout, r.stdout[-2000:]
 
 
 def test_sharded_recover_partials_sum_to_full():
