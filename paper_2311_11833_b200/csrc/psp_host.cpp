@@ -102,6 +102,7 @@ struct psp_ctx {
   DevBuf wptr_d, wlane_d, wval_d, flag_d;
   // fast combination layout (every row a contiguous run of <= 16 lanes in one 32-lane block)
   bool w_seg = false;
+  int32_t w_uni = 0;            // L when weight row w is lanes [w*L, w*L+L) for every w
   bool recovered = false;
 
   // --- host-API staging ---
@@ -185,6 +186,7 @@ static void reset_numeric(psp_ctx* h) {
   h->wlane_d.release();
   h->wval_d.release();
   h->w_seg = false;
+  h->w_uni = 0;
   h->growth_d.release();
   h->offmax_d.release();
   h->K = h->K_pad = h->R = h->W = 0;
@@ -1064,6 +1066,14 @@ psp_status psp_set_weights(psp_handle h, int32_t W, const int32_t* w_ptr_h,
       ok = k1 - k0 == q1 - q0 - 1 && k0 / kBlock == k1 / kBlock && q1 - q0 <= 16;
     }
     h->w_seg = ok;
+    // uniform ladders (recover_uni_kernel): row w = lanes [w*L, w*L + L)
+    int32_t L = W > 0 ? ptr[1] - ptr[0] : 0;
+    bool uni = L == 2 || L == 4 || L == 8 || L == 16;
+    for (int32_t w = 0; w < W && uni; ++w) {
+      uni = ptr[w] == w * L && ptr[w + 1] == (w + 1) * L;
+      for (int32_t j = 0; j < L && uni; ++j) uni = lane[ptr[w] + j] == w * L + j;
+    }
+    h->w_uni = uni ? L : 0;
   }
   h->W = W;
   return PSP_OK;
@@ -1072,7 +1082,11 @@ psp_status psp_set_weights(psp_handle h, int32_t W, const int32_t* w_ptr_h,
 psp_status psp_recover(psp_handle h, double* x) {
   if (!h || !x) return PSP_ERR_ARG;
   if (!h->solved || h->W == 0) return fail(h, PSP_ERR_STATE, "solve_batch and set_weights first");
-  if (h->w_seg) {
+  if (h->w_uni) {
+    CUDA_TRY(h, psp::launch_recover_uni(h->plan, h->W, h->R, h->w_uni, (const double*)h->wval_d.p,
+                                        (const double*)h->X_d.p, (const int32_t*)h->status_d.p, x,
+                                        (int32_t*)h->flag_d.p, h->stream));
+  } else if (h->w_seg) {
     CUDA_TRY(h, psp::launch_recover_seg(h->plan, h->W, h->R, (const int32_t*)h->wptr_d.p,
                                         (const int32_t*)h->wlane_d.p, (const double*)h->wval_d.p,
                                         (const double*)h->X_d.p, (const int32_t*)h->status_d.p, x,

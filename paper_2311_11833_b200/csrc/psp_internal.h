@@ -140,6 +140,9 @@ cudaError_t launch_recover(const DevicePlan& p, int32_t W, int32_t R, const int3
                            const int32_t* w_lane, const double* w_val, const double* X,
                            const int32_t* status, double* x_out, int32_t* infeasible_flag,
                            cudaStream_t stream);
+cudaError_t launch_recover_uni(const DevicePlan& p, int32_t W, int32_t R, int32_t L,
+                               const double* w_val, const double* X, const int32_t* status,
+                               double* x_out, int32_t* flag, cudaStream_t stream);
 cudaError_t launch_recover_seg(const DevicePlan& p, int32_t W, int32_t R, const int32_t* w_ptr,
                                const int32_t* w_lane, const double* w_val, const double* X,
                                const int32_t* status, double* x_out, int32_t* flag,

@@ -132,6 +132,43 @@ def test_failure_modes():
     assert np.array_equal(g["status"], sto) and g["status"][0] != 0
 
 
+@pytest.mark.parametrize("L", [2, 4, 8, 16])
+def test_uniform_ladder_recover_matches_general_path(L):
+    """Row w = lanes [w*L, w*L+L) takes recover_uni_kernel; appending an empty row makes
+    the same weights non-uniform (recover_seg_kernel).  Both bitwise equal, within 1e-10
+    of the oracle's combination, NaN + BATCH_INFEASIBLE on the rows holding a failed
+    lane (S:L270)."""
+    w = config(1)
+    s = w.system()
+    rng = np.random.default_rng(70 + L)
+    K = 6 * 32 + L  # several blocks, ragged tail
+    eps = rng.choice([-1, 1], K) * 10.0 ** rng.uniform(-4, -2, K)
+    eps[L + 1] = 0.0  # unperturbed lane with a leading zero pivot: fails (P:L304)
+    W = K // L
+    wv = rng.normal(size=W * L)
+    wp = np.arange(W + 1, dtype=np.int32) * L
+    wl = np.arange(W * L, dtype=np.int32)
+    B = np.stack([s.b[:, 0], rng.normal(size=s.n)], axis=1)
+    g = gpu_run(s, eps, "mindeg_first", s.slot_p, 0.0, B=B, w_csr=(wp, wl, wv))
+    solver = g["solver"]
+    solver.psp_set_weights(np.r_[wp, wp[-1]].astype(np.int32), wl, wv)
+    xg = solver.psp_recover().cpu().numpy()
+    solver.close()
+    xu = g["xhat"]
+    assert xu.shape == (W, 2, s.n) and xg.shape == (W + 1, 2, s.n)
+    assert np.array_equal(xu, xg[:W], equal_nan=True) and (xg[W] == 0).all()
+    assert g["rc"] == psp.PSP_ERR_BATCH_INFEASIBLE
+    Xo, sto = oracle.SparseOracle(s, g["operm"]).batch(eps, 0.0, B)
+    assert np.array_equal(g["status"], sto) and sto[L + 1] != 0
+    Wm = np.zeros((W, K))
+    for r in range(W):
+        Wm[r, r * L:(r + 1) * L] = wv[r * L:(r + 1) * L]
+    bad = 1  # row holding lane L+1
+    assert np.isnan(xu[bad]).all() and np.isfinite(np.delete(xu, bad, axis=0)).all()
+    xo = oracle.combine(np.delete(Wm, bad, axis=0), np.nan_to_num(Xo))
+    assert rel(np.delete(xu, bad, axis=0), xo) <= 1e-10
+
+
 def test_default_pivot_tol_and_lane_independence():
     w = config(1)
     s = w.system()
