@@ -294,6 +294,18 @@ psp_status psp_solve_host_async(psp_handle h, const double* A_vals_h, int32_t R,
  * psp_solve_host_async). */
 psp_status psp_synchronize(psp_handle h);
 
+/* Optional error test ("Optionally, test the solution error",
+ * P:L323): res_h[w * R + r] = || A x[w][r] - B[:, r] ||_2 for W x R candidate
+ * solutions.  A_vals (device, nnz_A, CSR order of the analysed pattern), B (device,
+ * n x R col-major, leading dimension n), x (device, W x R x n, ORIGINAL ordering, e.g.
+ * psp_recover's output).  Row i: t_i = (sum_q A_q x_{c_q}, ascending q, fma) - b_i;
+ * the squares are summed per thread in ascending i and then over a fixed tree, so
+ * the result is deterministic (not the oracle's summation order: parity within a
+ * relative 1e-12 of ||A|| ||x|| + ||b||).  Non-finite x gives a non-finite residual.
+ * Synchronous.  Errors: ARG (W < 1, R < 1, null), STATE (symbolic_analyse first), CUDA. */
+psp_status psp_residual(psp_handle h, const double* A_vals, int32_t W, int32_t R, const double* B,
+                        const double* x, double* res_h);
+
 /* ---- host helper (pure) --------------------------------------------------------- */
 
 /* Paper ladder (Remark 2): for m magnitudes s_h[j] (distinct, non-zero),

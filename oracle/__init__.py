@@ -8,7 +8,8 @@ arXiv 2311.11833 computes (Alg. 1):
      (oracle.c: dense OR1, and sparse OR2 for sizes where O(n^3) is infeasible);
   3-4. combine the lanes with the weights of Remark 2 / Eq. (13) (weights.py,
      exact rationals; oracle.c: oracle_combine);
-  5. optional error test: residual ||A x - b|| and the partial-pivot x* (oracle.c).
+  5. optional error test: residual ||A x - b|| (residual(), row by row) and the
+     partial-pivot x* (oracle.c).
 
 Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
 reference leg may import this package.  It shares no code with the CUDA path
@@ -237,6 +238,24 @@ def reference_solve(sysm, B=None):
                                       _p(_c(sysm.col_idx, np.int32)), _p(_c(sysm.vals, np.float64)),
                                       R, _p(Bc), _p(X))
     return X, st
+
+
+def residual(sysm, X, B=None):
+    """Alg. 1's optional error test: ||A x - b||_2 for every
+    x = X[w, r] ([W, R, n], original ordering) against b = B[:, r] (default sysm.b):
+    the definition written out row by row over the CSR entries.  -> [W, R]."""
+    B = sysm.b if B is None else B
+    X = np.asarray(X, dtype=np.float64)
+    W, R, n = X.shape
+    out = np.empty((W, R))
+    for w in range(W):
+        for r in range(R):
+            t = np.empty(n)
+            for i in range(n):
+                q0, q1 = sysm.row_ptr[i], sysm.row_ptr[i + 1]
+                t[i] = np.dot(sysm.vals[q0:q1], X[w, r, sysm.col_idx[q0:q1]]) - B[i, r]
+            out[w, r] = np.linalg.norm(t)
+    return out
 
 
 def combine(weights_WK, X):

@@ -81,6 +81,9 @@ struct psp_ctx {
   bool growth = false;
   DevBuf growth_d, offmax_d;
   const uint8_t* isdiag_d = nullptr;   // plan buffer: CSR entry is a diagonal entry
+  const int32_t* rowptr_d = nullptr;   // plan buffers: the analysed CSR pattern (psp_residual)
+  const int32_t* colidx_d = nullptr;
+  DevBuf res_d;                        // psp_residual output
   std::vector<cudaEvent_t> fev, sev;
   size_t nf = 0, ns = 0;
 
@@ -171,6 +174,7 @@ static void release_plan(psp_ctx* h) {
   h->plan_bufs.clear();
   h->plan = DevicePlan{};
   h->isdiag_d = nullptr;
+  h->rowptr_d = h->colidx_d = nullptr;
 }
 
 static void reset_numeric(psp_ctx* h) {
@@ -543,6 +547,10 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
     for (int32_t r = 0; r < n; ++r)
       for (int32_t q = row_ptr_h[r]; q < row_ptr_h[r + 1]; ++q) isdiag[q] = col_idx_h[q] == r;
     if (!host_only && (s = upload(h, isdiag, &h->isdiag_d))) return s;
+    std::vector<int32_t> rp(row_ptr_h, row_ptr_h + n + 1), ci(col_idx_h, col_idx_h + nnzA);
+    if (ci.empty()) ci.push_back(0);
+    if (!host_only && (s = upload(h, rp, &h->rowptr_d))) return s;
+    if (!host_only && (s = upload(h, ci, &h->colidx_d))) return s;
   }
 #undef UP
   if (!psp::choose_launch(P, h->launch, (int)h->opt_groups, (int)h->opt_warps,
@@ -1098,6 +1106,21 @@ psp_status psp_recover(psp_handle h, double* x) {
                                     (int32_t*)h->flag_d.p, h->stream));
   }
   h->recovered = true;
+  return PSP_OK;
+}
+
+psp_status psp_residual(psp_handle h, const double* A_vals, int32_t W, int32_t R, const double* B,
+                        const double* x, double* res_h) {
+  if (!h || !A_vals || !B || !x || !res_h || W < 1 || R < 1) return PSP_ERR_ARG;
+  if (!h->rowptr_d) return fail(h, PSP_ERR_STATE, "symbolic_analyse first");
+  cudaSetDevice(h->device);
+  psp_status s;
+  if ((s = ensure(h, h->res_d, sizeof(double) * (size_t)W * R))) return s;
+  CUDA_TRY(h, psp::launch_residual(h->n, h->rowptr_d, h->colidx_d, A_vals, W, R, B, x,
+                                   (double*)h->res_d.p, h->stream));
+  CUDA_TRY(h, cudaMemcpyAsync(res_h, h->res_d.p, sizeof(double) * (size_t)W * R,
+                              cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   return PSP_OK;
 }
 

@@ -130,6 +130,9 @@ cudaError_t launch_factor(const DevicePlan& p, const LaunchInfo& li, const int32
                           double* gscratch, double* gscr, int32_t* status, int32_t K_pad,
                           double* Y, cudaStream_t stream);
 // g_k = max|U| / max|A_k| per lane, from the factor in V (growth monitoring)
+cudaError_t launch_residual(int32_t n, const int32_t* row_ptr, const int32_t* col_idx,
+                            const double* A, int32_t W, int32_t R, const double* B, const double* x,
+                            double* res, cudaStream_t stream);
 cudaError_t launch_growth(const DevicePlan& p, const LaunchInfo& li, const double* V, const double* A,
                           const uint8_t* isdiag, const double* eps, const double* dperm, int32_t K,
                           double* offmax_scratch, double* growth, cudaStream_t stream);

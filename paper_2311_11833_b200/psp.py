@@ -25,7 +25,7 @@ EXPORTS = ["psp_create", "psp_destroy", "psp_set_stream", "psp_status_string",
            "psp_set_perturbations", "psp_factor_batch", "psp_solve_batch", "psp_factor_solve_batch",
            "psp_get_solutions", "psp_get_phase_times", "psp_get_lane_growth", "psp_estimate_rho",
            "psp_set_weights", "psp_recover", "psp_get_lane_status", "psp_solve_host", "psp_solve_host_async",
-           "psp_synchronize", "psp_ladder_weights", "psp_set_option", "psp_get_factor"]
+           "psp_synchronize", "psp_ladder_weights", "psp_set_option", "psp_get_factor", "psp_residual"]
 OPT = {"factor_groups": 1, "factor_warps": 2, "factor_lanes": 3, "factor_slab_warps": 4,
        "factor_pairs": 5, "factor_tmem": 6, "solve_tmem": 7, "phase_events": 8, "growth": 9, "coop": 10}
 
@@ -78,6 +78,7 @@ def lib():
             "psp_get_phase_times": [P, P],
             "psp_get_lane_growth": [P, P],
             "psp_estimate_rho": [P, I32, I32, D, P, P, P, P],
+            "psp_residual": [P, P, I32, I32, P, P, P],
             "psp_get_solutions": [P, P],
             "psp_set_weights": [P, I32, P, P, P],
             "psp_recover": [P, P],
@@ -215,6 +216,20 @@ class Solver:
                                            ctypes.byref(rho), ctypes.byref(it), ctypes.byref(conv)))
         self.R = 1
         return rho.value, it.value, bool(conv.value)
+
+    def psp_residual(self, A_vals, B, x):
+        """||A x[w][r] - B[r]||_2 for x device float64 [W, R, n] (original ordering, e.g.
+        psp_recover's output), B device float64 [R, n]; returns numpy [W, R] (psp.h)."""
+        self._check_dev(A_vals, self.torch.float64, (self.nnz_A,))
+        self._check_dev(B, self.torch.float64, None)
+        self._check_dev(x, self.torch.float64, None)
+        R, n = B.shape
+        assert n == self.n and B.is_contiguous() and x.is_contiguous()
+        assert x.dim() == 3 and x.shape[1] == R and x.shape[2] == n
+        W = x.shape[0]
+        res = np.empty((W, R), dtype=np.float64)
+        self._check(lib().psp_residual(self.h, _t_ptr(A_vals), W, R, _t_ptr(B), _t_ptr(x), _np_ptr(res)))
+        return res
 
     def psp_get_lane_growth(self):
         """g_k = max|U_k| / max|A_k| of the last factorisation (growth option on)."""

@@ -169,6 +169,40 @@ def test_uniform_ladder_recover_matches_general_path(L):
     assert rel(np.delete(xu, bad, axis=0), xo) <= 1e-10
 
 
+@pytest.mark.parametrize("ci", [0, 1])
+def test_residual_matches_oracle(ci):
+    """psp_residual (a7) on the recovered rows, a zero row (-> ||b||) and a NaN
+    row, two right-hand sides: within 1e-12 (||A|| ||x|| + ||b||) of the oracle's
+    row-by-row residual; the recovered solutions' residuals are small (the method's
+    O(eps^2m) accuracy, P:L323)."""
+    w = config(ci)
+    s = w.system()
+    rng = np.random.default_rng(90 + ci)
+    B = np.stack([s.b[:, 0], rng.normal(size=s.n)], axis=1)
+    g = gpu_run(s, w.eps(), B=B, ladders=w.ladders)
+    assert (g["status"] == 0).all()
+    solver = g["solver"]
+    xh = torch.tensor(g["xhat"], dtype=torch.float64, device="cuda")
+    extra = torch.zeros((2, 2, s.n), dtype=torch.float64, device="cuda")
+    extra[1, :, 3] = float("nan")
+    x = torch.cat([xh, extra]).contiguous()
+    A = torch.tensor(s.vals, dtype=torch.float64, device="cuda")
+    Bt = torch.tensor(B.T.copy(), dtype=torch.float64, device="cuda")
+    res = solver.psp_residual(A, Bt, x)
+    solver.close()
+    xc = x.cpu().numpy()
+    W = xh.shape[0]
+    ro = oracle.residual(s, xc[:W + 1], B)
+    anorm = np.abs(s.vals).sum()
+    for wi in range(W + 1):
+        for r in range(2):
+            scale = anorm * np.linalg.norm(xc[wi, r]) + np.linalg.norm(B[:, r])
+            assert abs(res[wi, r] - ro[wi, r]) <= 1e-12 * scale
+    assert np.allclose(res[W], np.linalg.norm(B, axis=0), rtol=1e-14, atol=0)
+    assert np.isnan(res[W + 1]).all()
+    assert (res[:W, 0] <= 1e-6 * np.linalg.norm(B[:, 0])).all()
+
+
 def test_default_pivot_tol_and_lane_independence():
     w = config(1)
     s = w.system()

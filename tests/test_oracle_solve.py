@@ -314,3 +314,29 @@ def test_power_rho_pins():
     lam = np.max(np.abs(np.linalg.eigvals(np.linalg.solve(M, np.diag(dd)))))
     r, it, conv = oracle.power_rho(_Tiny(M, dd, np.ones(n)), np.ones(n), max_iter=5000, rtol=1e-13)
     assert abs(r - lam) <= 1e-8 * lam
+
+
+def test_residual_pins():
+    """Alg. 1 optional error test: a hand-computed 2x2 case, x = 0 gives ||b||,
+    the partial-pivot x* gives a rounding-level residual, and x* + delta e_j gives
+    |delta| ||A e_j|| (linearity)."""
+    from types import SimpleNamespace
+    # A = [[2, 1], [0, 3]], x = [1, 1], b = [1, 1]: A x - b = [2, 2] -> 2 sqrt 2
+    t = SimpleNamespace(n=2, row_ptr=np.array([0, 2, 3]), col_idx=np.array([0, 1, 1]),
+                        vals=np.array([2.0, 1.0, 3.0]), b=np.ones((2, 1)))
+    assert oracle.residual(t, np.ones((1, 1, 2)))[0, 0] == 2.0 * np.sqrt(2.0)
+    s = config(1).system()
+    n = s.n
+    assert oracle.residual(s, np.zeros((1, 1, n)))[0, 0] == np.linalg.norm(s.b[:, 0])
+    xs, st = oracle.reference_solve(s)
+    assert st == 0
+    r0 = oracle.residual(s, xs[None])[0, 0]
+    Ad = np.zeros((n, n))
+    for i in range(n):
+        Ad[i, s.col_idx[s.row_ptr[i]:s.row_ptr[i + 1]]] = s.vals[s.row_ptr[i]:s.row_ptr[i + 1]]
+    assert r0 <= 1e-12 * np.linalg.norm(Ad) * np.linalg.norm(xs)
+    j, delta = 7, 1e-3
+    xp = xs.copy()
+    xp[0, j] += delta
+    rp = oracle.residual(s, xp[None])[0, 0]
+    assert abs(rp - delta * np.linalg.norm(Ad[:, j])) <= 1e-6 * rp
