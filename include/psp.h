@@ -294,6 +294,22 @@ psp_status psp_solve_host_async(psp_handle h, const double* A_vals_h, int32_t R,
  * psp_solve_host_async). */
 psp_status psp_synchronize(psp_handle h);
 
+/* Re-perturbation of failed ladders (a perturbed lane
+ * can still meet a (near-)zero pivot; another perturbation size avoids it).  After a
+ * factorisation, every weight row of psp_set_weights holding a failed lane (status != 0)
+ * has the eps of all its lanes multiplied by `scale`; other lanes keep theirs.  The
+ * paper's weights (Remark 2: beta_j depends only on ratios of the squared magnitudes)
+ * are invariant under a common scale of a ladder, so the rows' weights stay valid —
+ * caller-supplied weights that are not scale-invariant must be reset by the caller.
+ * n_rows_h (may be NULL) = rows rescaled.  When a row was rescaled the factorisation is
+ * invalidated: the caller factors again (same A_vals).  Synchronous (reads the
+ * statuses).  Errors: ARG (scale zero or non-finite), STATE (factor_batch and
+ * set_weights first), CUDA. */
+psp_status psp_rescale_failed_rows(psp_handle h, double scale, int32_t* n_rows_h);
+
+/* The handle's current eps[K] (after psp_rescale_failed_rows).  Errors: ARG, STATE. */
+psp_status psp_get_perturbations(psp_handle h, double* eps_h);
+
 /* Optional error test ("Optionally, test the solution error",
  * P:L323): res_h[w * R + r] = || A x[w][r] - B[:, r] ||_2 for W x R candidate
  * solutions.  A_vals (device, nnz_A, CSR order of the analysed pattern), B (device,

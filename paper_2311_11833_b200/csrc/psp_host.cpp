@@ -93,6 +93,8 @@ struct psp_ctx {
   bool factored = false;
   bool growth_valid = false;
   std::vector<double> d_host;   // D's diagonal, original ordering (psp_estimate_rho)
+  std::vector<double> eps_host; // eps of the K lanes (psp_rescale_failed_rows)
+  std::vector<int32_t> wptr_host, wlane_host;   // the stored weight rows (same)
   DevBuf rho_r_d, rho_x_d;      // psp_estimate_rho: right-hand side D v, recovered rows
 
   // --- solve ---
@@ -738,6 +740,7 @@ psp_status psp_set_perturbations(psp_handle h, int32_t K, const double* eps_h, c
   h->K = K;
   h->K_pad = Kp;
   h->d_host.assign(d_h, d_h + h->n);
+  h->eps_host.assign(eps_h, eps_h + K);
   h->factored = h->solved = h->recovered = false;
   return PSP_OK;
 }
@@ -1083,7 +1086,48 @@ psp_status psp_set_weights(psp_handle h, int32_t W, const int32_t* w_ptr_h,
     }
     h->w_uni = uni ? L : 0;
   }
+  h->wptr_host = ptr;
+  h->wlane_host = lane;
   h->W = W;
+  return PSP_OK;
+}
+
+psp_status psp_rescale_failed_rows(psp_handle h, double scale, int32_t* n_rows_h) {
+  if (!h) return PSP_ERR_ARG;
+  if (!(scale != 0.0) || !std::isfinite(scale)) return fail(h, PSP_ERR_ARG, "scale must be finite and non-zero");
+  if (!h->factored || h->W == 0) return fail(h, PSP_ERR_STATE, "factor_batch and set_weights first");
+  cudaSetDevice(h->device);
+  const int32_t K = h->K, Kp = h->K_pad;
+  std::vector<int32_t> st(K);
+  CUDA_TRY(h, cudaMemcpyAsync(st.data(), h->status_d.p, sizeof(int32_t) * K, cudaMemcpyDeviceToHost,
+                              h->stream));
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  std::vector<uint8_t> mark(K, 0);
+  int32_t rows = 0;
+  for (int32_t w = 0; w < h->W; ++w) {
+    bool bad = false;
+    for (int32_t q = h->wptr_host[w]; q < h->wptr_host[w + 1] && !bad; ++q)
+      bad = h->wlane_host[q] < K && st[h->wlane_host[q]] != 0;
+    if (!bad) continue;
+    ++rows;
+    for (int32_t q = h->wptr_host[w]; q < h->wptr_host[w + 1]; ++q)
+      if (h->wlane_host[q] < K) mark[h->wlane_host[q]] = 1;
+  }
+  if (n_rows_h) *n_rows_h = rows;
+  if (rows == 0) return PSP_OK;
+  for (int32_t k = 0; k < K; ++k)
+    if (mark[k]) h->eps_host[k] *= scale;
+  std::vector<double> eps(Kp);
+  for (int32_t k = 0; k < Kp; ++k) eps[k] = h->eps_host[k < K ? k : K - 1];
+  CUDA_TRY(h, cudaMemcpy(h->eps_d.p, eps.data(), sizeof(double) * Kp, cudaMemcpyHostToDevice));
+  h->factored = h->solved = h->recovered = false;
+  return PSP_OK;
+}
+
+psp_status psp_get_perturbations(psp_handle h, double* eps_h) {
+  if (!h || !eps_h) return PSP_ERR_ARG;
+  if (h->K == 0) return fail(h, PSP_ERR_STATE, "set_perturbations first");
+  std::copy(h->eps_host.begin(), h->eps_host.end(), eps_h);
   return PSP_OK;
 }
 

@@ -25,7 +25,8 @@ EXPORTS = ["psp_create", "psp_destroy", "psp_set_stream", "psp_status_string",
            "psp_set_perturbations", "psp_factor_batch", "psp_solve_batch", "psp_factor_solve_batch",
            "psp_get_solutions", "psp_get_phase_times", "psp_get_lane_growth", "psp_estimate_rho",
            "psp_set_weights", "psp_recover", "psp_get_lane_status", "psp_solve_host", "psp_solve_host_async",
-           "psp_synchronize", "psp_ladder_weights", "psp_set_option", "psp_get_factor", "psp_residual"]
+           "psp_synchronize", "psp_ladder_weights", "psp_set_option", "psp_get_factor", "psp_residual",
+           "psp_rescale_failed_rows", "psp_get_perturbations"]
 OPT = {"factor_groups": 1, "factor_warps": 2, "factor_lanes": 3, "factor_slab_warps": 4,
        "factor_pairs": 5, "factor_tmem": 6, "solve_tmem": 7, "phase_events": 8, "growth": 9, "coop": 10}
 
@@ -79,6 +80,8 @@ def lib():
             "psp_get_lane_growth": [P, P],
             "psp_estimate_rho": [P, I32, I32, D, P, P, P, P],
             "psp_residual": [P, P, I32, I32, P, P, P],
+            "psp_rescale_failed_rows": [P, D, P],
+            "psp_get_perturbations": [P, P],
             "psp_get_solutions": [P, P],
             "psp_set_weights": [P, I32, P, P, P],
             "psp_recover": [P, P],
@@ -230,6 +233,18 @@ class Solver:
         res = np.empty((W, R), dtype=np.float64)
         self._check(lib().psp_residual(self.h, _t_ptr(A_vals), W, R, _t_ptr(B), _t_ptr(x), _np_ptr(res)))
         return res
+
+    def psp_rescale_failed_rows(self, scale):
+        """Multiply the eps of every weight row holding a failed lane by `scale`;
+        returns the number of rows rescaled (factor again afterwards; psp.h)."""
+        n = ctypes.c_int32()
+        self._check(lib().psp_rescale_failed_rows(self.h, float(scale), ctypes.byref(n)))
+        return n.value
+
+    def psp_get_perturbations(self):
+        eps = np.empty(self.K, dtype=np.float64)
+        self._check(lib().psp_get_perturbations(self.h, _np_ptr(eps)))
+        return eps
 
     def psp_get_lane_growth(self):
         """g_k = max|U_k| / max|A_k| of the last factorisation (growth option on)."""

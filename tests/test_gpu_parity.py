@@ -203,6 +203,58 @@ def test_residual_matches_oracle(ci):
     assert (res[:W, 0] <= 1e-6 * np.linalg.norm(B[:, 0])).all()
 
 
+@pytest.mark.parametrize("ci", [0, 1])
+def test_rescale_failed_ladders(ci):
+    """SURVEY 8(f) 1 re-perturbation: with the zero-diagonal slot eliminated first its
+    pivot is eps_k d exactly, so an absolute tolerance fails the small-eps lanes; every
+    ladder holding a failed lane is rescaled by 20 (Remark 2 weights are scale-invariant),
+    refactored, and then statuses equal the oracle's on the new eps (bit-exact) and the
+    recovered x is within 1e-10 of the oracle's combination."""
+    w = config(ci)
+    s = w.system()
+    ladders = [np.array([1e-4, 2e-4]), np.array([2e-3, 4e-3]), np.array([5e-4, 3e-3]),
+               np.array([3e-3, 6e-3, 9e-3])]
+    eps = np.concatenate([ladder_eps(m) for m in ladders])
+    dslot = abs(s.d[s.slot_p])
+    tol = 1.5e-3 * dslot
+    solver = psp.Solver(0)
+    solver.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering="mindeg_first", first_node=s.slot_p)
+    info, perm = solver.psp_get_symbolic_info()
+    operm = oracle_perm(s, s.slot_p)
+    assert np.array_equal(perm, operm)
+    solver.psp_set_perturbations(eps, s.d)
+    wp, wl, wv = psp.ladder_weights_csr(ladders)
+    solver.psp_set_weights(wp, wl, wv)
+    A = torch.tensor(s.vals, dtype=torch.float64, device="cuda")
+    Bt = torch.tensor(s.b.T.copy(), dtype=torch.float64, device="cuda")
+    st = torch.empty(len(eps), dtype=torch.int32, device="cuda")
+    solver.psp_factor_batch(A, tol, st)
+    st0 = st.cpu().numpy()
+    _, sto = oracle.SparseOracle(s, operm).batch(eps, tol)
+    assert np.array_equal(st0, sto) and (st0 != 0).any() and (st0 == 0).any()
+    # expected new eps, from the statuses and the ladder rows (lanes [wp[r], wp[r+1]))
+    exp = eps.copy()
+    rows = 0
+    for r in range(len(wp) - 1):
+        if (st0[wl[wp[r]:wp[r + 1]]] != 0).any():
+            exp[wl[wp[r]:wp[r + 1]]] *= 20.0
+            rows += 1
+    assert solver.psp_rescale_failed_rows(20.0) == rows == 2
+    eps1 = solver.psp_get_perturbations()
+    assert np.array_equal(eps1, exp)
+    solver.psp_factor_batch(A, tol, st)
+    solver.psp_solve_batch(Bt)
+    xh = solver.psp_recover().cpu().numpy()
+    rc, st1 = solver.psp_get_lane_status()
+    X = solver.psp_get_solutions().cpu().numpy()
+    solver.close()
+    Xo, sto1 = oracle.SparseOracle(s, operm).batch(eps1, tol)
+    assert np.array_equal(st1, sto1) and (st1 == 0).all() and rc == psp.PSP_OK
+    assert np.array_equal(X, Xo)
+    xo = oracle.combine(oracle.ladder_weight_matrix(ladders), Xo)
+    assert rel(xh, xo) <= 1e-10
+
+
 def test_default_pivot_tol_and_lane_independence():
     w = config(1)
     s = w.system()
