@@ -77,3 +77,18 @@ def test_lane_weights_layout():
     lw = weights.lane_weights([1.0, 2.0])
     assert lw == [2 / 3, 2 / 3, -1 / 6, -1 / 6]
     assert abs(sum(lw) - 1.0) < 1e-15
+
+
+def test_beta_invariant_under_common_scale():
+    """Basis of psp_rescale_failed_rows: beta = (Gamma_m^T)^-1 e_1 (Eq. (13)) depends only
+    on ratios of the squared nodes, so scaling a whole ladder leaves it unchanged —
+    exactly in rationals, and to rounding in the library's host helper."""
+    from fractions import Fraction
+    for nodes in ([1, 2, 3], [Fraction(1, 1000), Fraction(3, 1000)], [2, 5, 7, 11]):
+        for c in (Fraction(20), Fraction(1, 7), Fraction(-3)):
+            assert weights.beta_vandermonde(nodes) == weights.beta_vandermonde([c * x for x in nodes])
+    from paper_2311_11833_b200 import psp
+    s = np.array([1e-3, 2e-3, 3.5e-3])
+    _, w1 = psp.psp_ladder_weights(s)
+    _, w2 = psp.psp_ladder_weights(20.0 * s)
+    assert np.allclose(w1, w2, rtol=1e-14, atol=0)
