@@ -288,6 +288,42 @@ def test_identity_vs_normal_D_study():
         print(f"  {name:8s} " + "  ".join(f"{e:.2e}" for e in errs))
 
 
+@pytest.mark.parametrize("coop", [0, 2])
+def test_values_only_refactorisation_many_jacobians(coop):
+    """one symbolic analysis, several Jacobians with the same pattern
+    (values-only re-upload, e.g. the NR steps / V-starts of P:L302): each
+    factor_solve_batch on the same handle bitwise equal to the oracle on its values."""
+    w = config(1)
+    s = w.system()
+    ladders = [w.ladders[0] * f for f in np.linspace(0.5, 2.0, 12)]   # K = 96 lanes
+    eps = np.concatenate([ladder_eps(m) for m in ladders])
+    rng = np.random.default_rng(302)
+    solver = psp.Solver(0)
+    solver.psp_set_option("coop", coop)
+    solver.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering="mindeg")
+    info, perm = solver.psp_get_symbolic_info()
+    solver.psp_set_perturbations(eps, s.d)
+    solver.psp_set_weights(*psp.ladder_weights_csr(ladders))
+    b = torch.tensor(s.b[:, 0].copy(), dtype=torch.float64, device="cuda")
+    for j in range(3):
+        vals = s.vals * (1.0 + 0.1 * rng.normal(size=len(s.vals)))
+        A = torch.tensor(vals, dtype=torch.float64, device="cuda")
+        solver.psp_factor_solve_batch(A, b, 0.0)
+        xh = solver.psp_recover().cpu().numpy()
+        rc, st = solver.psp_get_lane_status()
+        X = solver.psp_get_solutions().cpu().numpy()
+        sj = w.system()
+        sj.vals = vals
+        assert len(eps) == 2 * sum(len(l) for l in ladders)
+        tol = oracle.default_tol(sj.n, sj.row_ptr, sj.col_idx, sj.vals)
+        Xo, sto = oracle.SparseOracle(sj, perm).batch(eps, tol, s.b[:, :1])
+        assert np.array_equal(st, sto) and np.array_equal(X[sto == 0], Xo[sto == 0])
+        if (sto == 0).all():
+            xo = oracle.combine(oracle.ladder_weight_matrix(ladders), Xo)
+            assert rel(xh, xo) <= 1e-10
+    solver.close()
+
+
 def test_default_pivot_tol_and_lane_independence():
     w = config(1)
     s = w.system()
