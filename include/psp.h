@@ -97,6 +97,11 @@ typedef struct {
   /* the augmented program of psp_factor_solve_batch ([A | b]): aug_ok = 2 fused, 1
    * available but slower (a weaker slot store: the call runs factor + solve), 0 none */
   int32_t aug_ok, aug_max_live, aug_warps_per_cta, aug_pend_smem;
+  /* capacity-planned programs (PSP_OPT_FACTOR_SPILL): spill_ok bit 0 plain, bit 1 augmented
+   * available; spill_cap = slots per lane; spill_ops = spill + reload operations per lane
+   * (plain program; aug_spill_ops for [A | b]); spill_entries = spill-area entries per lane;
+   * spill_warps_per_cta = warps of the 2-CTA-per-SM launch */
+  int32_t spill_ok, spill_cap, spill_ops, spill_entries, aug_spill_ops, spill_warps_per_cta;
 } psp_symbolic_info;
 
 /* ---- lifetime ---------------------------------------------------------------- */
@@ -138,14 +143,23 @@ psp_status psp_destroy(psp_handle h);
  *                         cooperative kernels (one CTA per system, its factor in shared
  *                         memory, etree-level steps); 1: always (when the
  *                         factor fits shared memory); 2: never.  Bitwise-neutral.
+ *  PSP_OPT_FACTOR_SPILL   0 (default): automatic — when the pending set exceeds 127 slots
+ *                         per lane and the batch needs more than one round of the plain
+ *                         launch, factor with the capacity-planned program (<= 127 slots,
+ *                         the entries with the furthest next use spilled to a per-lane
+ *                         global area and reloaded before their next use):
+ *                         2 CTAs x 7 warps per SM instead of 1 x 7-8; 1: always (when a
+ *                         launch fits); 2: never.  Bitwise-neutral.
  * Errors: ARG (STATE: PSP_OPT_PHASE_EVENTS on a host-only handle). */
 enum { PSP_OPT_FACTOR_GROUPS = 1, PSP_OPT_FACTOR_WARPS = 2, PSP_OPT_FACTOR_LANES = 3,
        PSP_OPT_FACTOR_SLAB_WARPS = 4, PSP_OPT_FACTOR_PAIRS = 5, PSP_OPT_FACTOR_TMEM = 6,
        PSP_OPT_SOLVE_TMEM = 7, PSP_OPT_PHASE_EVENTS = 8, PSP_OPT_GROWTH = 9,
-       PSP_OPT_COOP = 10 };
+       PSP_OPT_COOP = 10, PSP_OPT_FACTOR_SPILL = 11 };
 psp_status psp_set_option(psp_handle h, int32_t option, int64_t value);
 
-/* Rebind the handle to another stream of the same device. */
+/* Rebind the handle to another stream of the same device.  Synchronises the old stream
+ * first (the handle's programs, factor and staging buffers are reused by the next call,
+ * so work still queued on the old stream must not overlap it).  Errors: ARG, CUDA. */
 psp_status psp_set_stream(psp_handle h, void* cuda_stream);
 
 const char* psp_status_string(psp_status s);
@@ -237,10 +251,28 @@ psp_status psp_estimate_rho(psp_handle h, int32_t w, int32_t max_iter, double rt
  * STATE, CUDA. */
 psp_status psp_get_lane_growth(psp_handle h, double* growth_h);
 
-/* With PSP_OPT_PHASE_EVENTS on: device time (ms, cudaEventElapsedTime) of the last
- * factor kernel (ms_h[0]) and the last solve kernel (ms_h[1]) launched by the calls
- * above; synchronises on the last solve.  Errors: ARG, STATE, CUDA. */
+/* With PSP_OPT_PHASE_EVENTS on: the MEAN device time (ms, cudaEventElapsedTime between
+ * library events recorded on the handle's stream right before and after each launch) of
+ * the factor kernels (ms_h[0]) and of the solve kernels (ms_h[1]) launched since the
+ * previous psp_get_phase_times call (or since the option was switched on); 0 for a phase
+ * with no launch.  Resets the accumulation.  Synchronises on the recorded events.
+ * Errors: ARG, STATE, CUDA. */
 psp_status psp_get_phase_times(psp_handle h, float* ms_h);
+
+/* Which kernels the last numeric calls launched (introspection for tests and launch
+ * censuses): kernels_h[0] = factor kernel of the last factorisation,
+ * kernels_h[1] = 1 if it eliminated the augmented [A | b] (forward substitution fused),
+ * kernels_h[2] = solve kernel of the last solve, kernels_h[3] = 1 if that solve ran the
+ * forward pass (0: backward only, y came from the fused factor).  Kernel ids: PSP_KERNEL_*
+ * (0 = none launched yet).  Errors: ARG. */
+enum { PSP_KERNEL_NONE = 0,
+       PSP_KERNEL_COOP = 1,        /* cooperative small-batch kernels (CTA per system)      */
+       PSP_KERNEL_BATCH = 2,       /* batch kernels, slots in shared (or global) memory      */
+       PSP_KERNEL_BATCH_TMEM = 3,  /* batch kernels, slots in tensor memory + shared memory  */
+       PSP_KERNEL_BATCH_SPILL = 4  /* batch factor, capacity-planned slots (TMEM + shared)
+                                      with idle entries spilled to global memory            */
+};
+psp_status psp_get_last_kernels(psp_handle h, int32_t* kernels_h);
 
 /* Copy the per-lane solutions to X (device, K x R x n, lane-major, ORIGINAL
  * ordering): X[(k*R + r)*n + i] = x_k,r[i].  Errors: ARG, STATE. */
@@ -266,7 +298,8 @@ psp_status psp_set_weights(psp_handle h, int32_t W, const int32_t* w_ptr_h,
  * W x R x n.  With lanes sharded across GPUs this is the rank-local partial sum;
  * the caller reduces it (sum) across ranks.  A non-zero weight on a failed lane
  * yields NaN for that solution and raises the batch-infeasible flag
- * (psp_get_lane_status).  Errors: ARG, STATE, CUDA. */
+ * (psp_get_lane_status); the flag is cleared at the start of every psp_recover, so it
+ * always describes the last combination.  Errors: ARG, STATE, CUDA. */
 psp_status psp_recover(psp_handle h, double* x);
 
 /* Synchronise the stream and copy per-lane status to status_h[K] (may be NULL).

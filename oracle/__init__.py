@@ -240,6 +240,76 @@ def reference_solve(sysm, B=None):
     return X, st
 
 
+def _dense(sysm):
+    """A as a dense n x n array (CSR entries summed in place)."""
+    n = sysm.n
+    A = np.zeros((n, n))
+    for i in range(n):
+        for q in range(sysm.row_ptr[i], sysm.row_ptr[i + 1]):
+            A[i, sysm.col_idx[q]] += sysm.vals[q]
+    return A
+
+
+def pivoted_lanes(sysm, eps, B=None):
+    """x_k^piv = (A + eps_k D)^{-1} b by partial-pivot GE for every lane (SURVEY §8(c)
+    step 5: the floor of tolerance policy 3).  -> [K, R, n]."""
+    B = sysm.b if B is None else B
+    A = _dense(sysm)
+    d = np.asarray(sysm.d, dtype=np.float64)
+    out = np.empty((len(eps), B.shape[1], sysm.n))
+    for k, e in enumerate(eps):
+        LU, piv, st = lu_partial_pivot(A + float(e) * np.diag(d))
+        if st:
+            raise ValueError(f"lane {k}: singular perturbed matrix")
+        for r in range(B.shape[1]):
+            out[k, r] = lu_pp_solve(LU, piv, B[:, r])
+    return out
+
+
+def predicted_error(sysm, mags, B=None):
+    """Theorem 1's truncation error with its constant, exactly: the identity (I3) of
+    SURVEY §8(c) (Lagrange interpolation of t -> (I - t M^2)^{-1} x* at the nodes
+    t_j = s_j^2, evaluated at t = 0; Remark 2's beta are that Lagrange basis, P:L197-203;
+    Examples 1-2 are its leading terms):
+
+        x* - x_hat* = (-1)^m  prod_j [ t_j M^2 (I - t_j M^2)^{-1} ]  x*,   M = A^{-1} D,
+
+    for one ladder of m magnitudes s_j (lanes +-s_j, weights beta_j / 2).  Every operator
+    is applied through partial-pivot factorisations (lu_partial_pivot):
+      M v = A^{-1} (D v);
+      (I - t M^2)^{-1} v = 1/2 [(A + s D)^{-1} + (A - s D)^{-1}] (A v)   (the pair average
+        of Eq. (avg_hats), since (I + s M)^{-1} = (A + s D)^{-1} A).
+    The factors commute (functions of M^2); each step applies t_j M^2 (I - t_j M^2)^{-1}
+    so that neither prod t_j nor M^{2m} is formed on its own (no under/overflow for long
+    ladders).  Returns e_pred [R, n] (original ordering)."""
+    B = sysm.b if B is None else B
+    A = _dense(sysm)
+    d = np.asarray(sysm.d, dtype=np.float64)
+    LU, piv, st = lu_partial_pivot(A)
+    if st:
+        raise ValueError("singular A")
+
+    def M(v):
+        return lu_pp_solve(LU, piv, d * v)
+
+    pairs = []
+    for s in mags:
+        fp = lu_partial_pivot(A + float(s) * np.diag(d))
+        fm = lu_partial_pivot(A - float(s) * np.diag(d))
+        if fp[2] or fm[2]:
+            raise ValueError(f"singular A +- {s} D")
+        pairs.append((float(s), fp, fm))
+    out = np.empty((B.shape[1], sysm.n))
+    for r in range(B.shape[1]):
+        v = lu_pp_solve(LU, piv, B[:, r])          # x*
+        for s, fp, fm in pairs:
+            Av = A @ v
+            u = 0.5 * lu_pp_solve(fp[0], fp[1], Av) + 0.5 * lu_pp_solve(fm[0], fm[1], Av)
+            v = (s * s) * M(M(u))
+        out[r] = (-1.0) ** len(mags) * v
+    return out
+
+
 def residual(sysm, X, B=None):
     """Alg. 1's optional error test: ||A x - b||_2 for every
     x = X[w, r] ([W, R, n], original ordering) against b = B[:, r] (default sysm.b):

@@ -22,6 +22,7 @@
 
 using psp::DevicePlan;
 using psp::kBlock;
+using psp::kSpillCap;
 
 namespace {
 
@@ -68,6 +69,14 @@ struct psp_ctx {
   bool aug_fast = false;   // the augmented program keeps the plain one's slot store (TMEM /
                            // shared / global): psp_factor_solve_batch fuses, else it runs
                            // the two calls (measured: a store downgrade costs more)
+  // capacity-planned factor programs (plain and augmented): <= kSpillCap pending slots per
+  // lane, idle entries spilled to a global area; the TMEM kernel at 2 CTAs per SM
+  DevicePlan plan_spill, plan_spill_aug;
+  psp::LaunchInfo launch_spill, launch_spill_aug;
+  bool spill_ok = false, spill_aug_ok = false;
+  int32_t spill_stats[2][3] = {{0, 0, 0}, {0, 0, 0}};   // [plain, aug] x (spills, reloads, entries)
+  int64_t opt_spill = 0;           // PSP_OPT_FACTOR_SPILL: 0 automatic, 1 require, 2 off
+  DevBuf gspill_d;
   int64_t opt_groups = 0, opt_warps = 0, opt_lanes = 0, opt_slab_warps = 0;  // PSP_OPT_FACTOR_*
   int64_t opt_pairs = 1;                                                      // PSP_OPT_FACTOR_PAIRS
   int64_t opt_tmem = 0;                                                       // PSP_OPT_FACTOR_TMEM
@@ -109,6 +118,9 @@ struct psp_ctx {
   bool w_seg = false;
   int32_t w_uni = 0;            // L when weight row w is lanes [w*L, w*L+L) for every w
   bool recovered = false;
+
+  // kernels of the last numeric calls (psp_get_last_kernels)
+  int32_t last_factor = 0, last_factor_aug = 0, last_solve = 0, last_solve_fwd = 0;
 
   // --- host-API staging ---
   DevBuf stageA_d, stageB_d, stageX_d;
@@ -187,6 +199,7 @@ static void reset_numeric(psp_ctx* h) {
   h->X_d.release();
   h->fscratch_d.release();
   h->fscr_d.release();
+  h->gspill_d.release();
   h->sscratch_d.release();
   h->wptr_d.release();
   h->wlane_d.release();
@@ -297,6 +310,10 @@ psp_status psp_set_option(psp_handle h, int32_t option, int64_t value) {
       if (value < 0 || value > 2) return fail(h, PSP_ERR_ARG, "PSP_OPT_COOP must be 0, 1 or 2");
       h->opt_coop = value;
       return PSP_OK;
+    case PSP_OPT_FACTOR_SPILL:
+      if (value < 0 || value > 2) return fail(h, PSP_ERR_ARG, "PSP_OPT_FACTOR_SPILL must be 0, 1 or 2");
+      h->opt_spill = value;
+      return PSP_OK;
     case PSP_OPT_GROWTH:
       if (value != 0 && value != 1) return fail(h, PSP_ERR_ARG, "PSP_OPT_GROWTH must be 0 or 1");
       h->growth = value != 0;
@@ -332,6 +349,12 @@ psp_status psp_set_option(psp_handle h, int32_t option, int64_t value) {
 
 psp_status psp_set_stream(psp_handle h, void* cuda_stream) {
   if (!h) return PSP_ERR_ARG;
+  // the programs, factor and staging buffers are reused by the next call: finish the work
+  // queued on the old stream before a call on the new one can overwrite them
+  if (h->device >= 0) {
+    cudaSetDevice(h->device);
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  }
   h->stream = static_cast<cudaStream_t>(cuda_stream);
   return PSP_OK;
 }
@@ -493,6 +516,21 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
   HPa.aug = true;
   psp::build_programs(n, S.lcol, perm, row_ptr_h, col_idx_h, HP);
   psp::build_programs(n, S.lcol, perm, row_ptr_h, col_idx_h, HPa);
+  if (!HP.plan_ok || !HPa.plan_ok)
+    return fail(h, PSP_ERR_UNSUPPORTED, "internal: factor program failed its slot self-check");
+  // capacity-planned programs (spills) for the 2-CTA TMEM factor kernel
+  psp::HostPlan HPc, HPac;
+  HPc.fuse_pairs = HPac.fuse_pairs = h->opt_pairs != 0;
+  HPac.aug = true;
+  HPc.cap = HPac.cap = kSpillCap;
+  HPc.all_slots = HPac.all_slots = true;
+  const bool try_spill = h->opt_spill != 2 && (HP.f_slots > kSpillCap + 1 || h->opt_spill == 1);
+  if (try_spill) {
+    psp::build_programs(n, S.lcol, perm, row_ptr_h, col_idx_h, HPc);
+    psp::build_programs(n, S.lcol, perm, row_ptr_h, col_idx_h, HPac);
+    if (!HPc.plan_ok || !HPac.plan_ok)
+      return fail(h, PSP_ERR_UNSUPPORTED, "internal: capacity-planned program failed its slot self-check");
+  }
   psp::CoopPlan CP;
   psp::build_coop(n, S.lcol, perm, row_ptr_h, col_idx_h, HP, CP);
 
@@ -515,7 +553,7 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
   P.f_slots = HP.f_slots;
   P.f_chunk_words = HP.f_chunk_words;
   P.f_nchunks = (int32_t)(HP.f_stream.size() / HP.f_chunk_words);
-  P.c_scr = HP.c_max > psp::kFusedMax ? HP.c_max : 0;
+  P.c_scr = HP.c_max > psp::kFusedMax ? (HP.c_max + 3) & ~3 : 0;   // (rows padded to 4)
   P.f_npatch = (int32_t)HP.f_patch_pos.size();
   P.y_slots = HP.y_slots;
   P.x_slots = HP.x_slots;
@@ -647,7 +685,7 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
   Pa.f_slots = HPa.f_slots;
   Pa.f_chunk_words = HPa.f_chunk_words;
   Pa.f_nchunks = (int32_t)(HPa.f_stream.size() / HPa.f_chunk_words);
-  Pa.c_scr = HP.c_max + 1 > psp::kFusedMax ? HP.c_max + 1 : 0;
+  Pa.c_scr = HP.c_max + 1 > psp::kFusedMax ? (HP.c_max + 4) & ~3 : 0;
   Pa.f_npatch = (int32_t)HPa.f_patch_pos.size();
   psp::LaunchInfo la = h->launch;
   // (the augmented factor kernels exist for G = J = P = 1 only, and the factor they write
@@ -663,6 +701,37 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
   }
   h->plan_aug = Pa;
   h->launch_aug = la;
+  // capacity-planned variants (same V layout as the (1, 1, 1) launches: 32-lane slabs)
+  h->spill_ok = h->spill_aug_ok = false;
+  std::memset(h->spill_stats, 0, sizeof h->spill_stats);
+  if (try_spill && h->launch.f_groups == 1 && h->launch.f_lanes == 1 && h->launch.f_slab_warps == 1) {
+    for (int q = 0; q < 2; ++q) {
+      const psp::HostPlan& H = q ? HPac : HPc;
+      DevicePlan Pc = q ? Pa : P;
+      Pc.f_slots = H.f_slots;
+      Pc.f_chunk_words = H.f_chunk_words;
+      Pc.f_nchunks = (int32_t)(H.f_stream.size() / H.f_chunk_words);
+      Pc.c_scr = (H.c_scr_need + 3) & ~3;   // (scratch rows padded to 4: the compact
+                                             // update reads its columns in batches of 4)
+      Pc.f_npatch = (int32_t)H.f_patch_pos.size();
+      Pc.f_gspill = H.f_gspill;
+      psp::LaunchInfo lc = h->launch;
+      if (!psp::choose_launch_spill(Pc, lc, 0)) continue;
+      if (!host_only) {
+        if ((s = upload(h, H.f_stream, &Pc.f_stream))) return s;
+        if ((s = upload(h, H.f_patch_pos, &Pc.f_patch_pos))) return s;
+        if ((s = upload(h, H.f_patch_src, &Pc.f_patch_src))) return s;
+      }
+      (q ? h->plan_spill_aug : h->plan_spill) = Pc;
+      (q ? h->launch_spill_aug : h->launch_spill) = lc;
+      (q ? h->spill_aug_ok : h->spill_ok) = true;
+      h->spill_stats[q][0] = H.f_spills;
+      h->spill_stats[q][1] = H.f_reloads;
+      h->spill_stats[q][2] = H.f_gspill;
+    }
+  }
+  if (h->opt_spill == 1 && !h->spill_ok)
+    return fail(h, PSP_ERR_UNSUPPORTED, "PSP_OPT_FACTOR_SPILL = 1 but no capacity-planned launch fits");
   {
     auto store = [](const psp::LaunchInfo& li) { return li.f_tmem ? 2 : (li.f_pend_smem ? 1 : 0); };
     h->aug_fast = h->aug_ok && store(la) == store(h->launch);
@@ -711,6 +780,12 @@ psp_status psp_get_symbolic_info(psp_handle h, psp_symbolic_info* info, int32_t*
   info->aug_warps_per_cta = h->aug_ok ? h->launch_aug.f_warps : 0;
   info->aug_pend_smem = !h->aug_ok ? 0 : (h->launch_aug.f_tmem ? 2 : (h->launch_aug.f_pend_smem ? 1 : 0));
   info->births = h->f_births;
+  info->spill_ok = (h->spill_ok ? 1 : 0) | (h->spill_aug_ok ? 2 : 0);
+  info->spill_cap = kSpillCap;
+  info->spill_ops = h->spill_stats[0][0] + h->spill_stats[0][1];
+  info->spill_entries = h->spill_stats[0][2];
+  info->aug_spill_ops = h->spill_stats[1][0] + h->spill_stats[1][1];
+  info->spill_warps_per_cta = h->spill_ok ? h->launch_spill.f_warps : 0;
   if (perm_h) std::copy(h->perm.begin(), h->perm.end(), perm_h);
   return PSP_OK;
 }
@@ -721,7 +796,8 @@ psp_status psp_set_perturbations(psp_handle h, int32_t K, const double* eps_h, c
   if (!h->analysed) return fail(h, PSP_ERR_STATE, "psp_symbolic_analyse first");
   if (K < 1 || !eps_h || !d_h) return fail(h, PSP_ERR_ARG, "K >= 1, eps_h and d_h required");
   cudaSetDevice(h->device);
-  const int32_t Kp = (K + kBlock - 1) / kBlock * kBlock;
+  // (a multiple of 64: the capacity-planned factor gives a thread two 32-lane slabs)
+  const int32_t Kp = (K + 2 * kBlock - 1) / (2 * kBlock) * (2 * kBlock);
   std::vector<double> eps(Kp);
   for (int32_t k = 0; k < Kp; ++k) eps[k] = eps_h[k < K ? k : K - 1];  // pad: repeat last lane
   std::vector<double> dperm(h->n);
@@ -737,6 +813,13 @@ psp_status psp_set_perturbations(psp_handle h, int32_t K, const double* eps_h, c
   CUDA_TRY(h, cudaMemcpy(h->eps_d.p, eps.data(), sizeof(double) * Kp, cudaMemcpyHostToDevice));
   CUDA_TRY(h, cudaMemcpy(h->dperm_d.p, dperm.data(), sizeof(double) * h->n, cudaMemcpyHostToDevice));
   CUDA_TRY(h, cudaMemset(h->flag_d.p, 0, sizeof(int32_t)));
+  if (K != h->K) {   // weights were validated against the old lane count: drop them
+    h->W = 0;
+    h->w_seg = false;
+    h->w_uni = 0;
+    h->wptr_host.clear();
+    h->wlane_host.clear();
+  }
   h->K = K;
   h->K_pad = Kp;
   h->d_host.assign(d_h, d_h + h->n);
@@ -779,14 +862,27 @@ static psp_status phase_mark(psp_ctx* h, std::vector<cudaEvent_t>& pool, size_t&
 
 // Factorisation of the K perturbed copies with `plan` (aug = false) or of the augmented
 // [A | b] with `plan_aug` (aug = true: y = L^{-1} b goes to X).
+// The capacity-planned (spilling, 2 CTAs per SM) factor for this batch?  When it is
+// available and the batch needs more than one round of the plain launch (its extra
+// resident warps pay only then; PSP_OPT_FACTOR_SPILL overrides).
+static bool use_spill(psp_ctx* h, bool aug) {
+  if (h->opt_spill == 2 || !(aug ? h->spill_aug_ok : h->spill_ok)) return false;
+  if (h->opt_spill == 1) return true;
+  const psp::LaunchInfo& L = aug ? h->launch_aug : h->launch;
+  const int64_t round = (int64_t)h->n_sm * L.f_warps * std::max(1, L.f_ctas_per_sm);
+  return (int64_t)(h->K_pad / kBlock) > round;
+}
+
 static psp_status factor_impl(psp_handle h, const double* A_vals, double pivot_tol,
                               int32_t* lane_status, bool aug, const double* b) {
   if (!h) return PSP_ERR_ARG;
   if (!h->analysed || h->K == 0) return fail(h, PSP_ERR_STATE, "set_perturbations first");
   if (!A_vals) return fail(h, PSP_ERR_ARG, "A_vals required");
   if (!(pivot_tol == pivot_tol)) return fail(h, PSP_ERR_ARG, "pivot_tol is NaN");
-  const DevicePlan& P = aug ? h->plan_aug : h->plan;
-  const psp::LaunchInfo& LI = aug ? h->launch_aug : h->launch;
+  const bool spill = !use_coop(h) && use_spill(h, aug);
+  const DevicePlan& P = spill ? (aug ? h->plan_spill_aug : h->plan_spill) : (aug ? h->plan_aug : h->plan);
+  const psp::LaunchInfo& LI = spill ? (aug ? h->launch_spill_aug : h->launch_spill)
+                                    : (aug ? h->launch_aug : h->launch);
   cudaSetDevice(h->device);
   psp_status s;
   const double* tol_dev = nullptr;
@@ -817,6 +913,13 @@ static psp_status factor_impl(psp_handle h, const double* A_vals, double pivot_t
       if ((s = ensure(h, h->fscr_d, need))) return s;
     }
   }
+  if (spill) {
+    size_t need = sizeof(double) * (size_t)h->K_pad * std::max(1, P.f_gspill);
+    if (h->gspill_d.bytes < need) {
+      CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+      if ((s = ensure(h, h->gspill_d, need))) return s;
+    }
+  }
   if (h->phase_events) {
     if ((s = phase_mark(h, h->fev, h->nf))) return s;
   }
@@ -826,15 +929,20 @@ static psp_status factor_impl(psp_handle h, const double* A_vals, double pivot_t
     if ((s = ensure(h, h->offmax_d, sizeof(double)))) return s;
   }
   if (use_coop(h)) {   // (the augmented program is not needed: the solve does its forward)
+    h->last_factor = PSP_KERNEL_COOP;
+    h->last_factor_aug = 0;
     CUDA_TRY(h, psp::launch_coop_factor(h->plan, h->coop, A_vals, (const double*)h->eps_d.p,
                                         (const double*)h->dperm_d.p, tol_dev, pivot_tol,
                                         (double*)h->V_d.p, (int32_t*)h->status_d.p, h->K,
                                         kBlock / h->launch.f_groups * h->launch.f_lanes, h->stream));
   } else {
+    h->last_factor = spill ? PSP_KERNEL_BATCH_SPILL : (LI.f_tmem ? PSP_KERNEL_BATCH_TMEM : PSP_KERNEL_BATCH);
+    h->last_factor_aug = aug ? 1 : 0;
     CUDA_TRY(h, psp::launch_factor(P, LI, P.f_stream, (const double*)h->eps_d.p, tol_dev, pivot_tol,
                                    (double*)h->V_d.p, (double*)h->fscratch_d.p, (double*)h->fscr_d.p,
                                    (int32_t*)h->status_d.p, h->K_pad,
-                                   aug ? (double*)h->X_d.p : nullptr, h->stream));
+                                   aug ? (double*)h->X_d.p : nullptr, (double*)h->gspill_d.p,
+                                   h->stream));
   }
   if (h->phase_events) {
     if ((s = phase_mark(h, h->fev, h->nf))) return s;
@@ -875,7 +983,8 @@ psp_status psp_factor_solve_batch(psp_handle h, const double* A_vals, const doub
   if (!h) return PSP_ERR_ARG;
   if (!b) return fail(h, PSP_ERR_ARG, "b required");
   psp_status s;
-  if (h->analysed && (!h->aug_fast || use_coop(h))) {   // the two calls (bitwise the same)
+  const bool fuse = h->analysed && !use_coop(h) && (use_spill(h, true) || h->aug_fast);
+  if (h->analysed && !fuse) {   // the two calls (bitwise the same)
     if ((s = factor_impl(h, A_vals, pivot_tol, lane_status, false, nullptr))) return s;
     return psp_solve_batch(h, 1, b, h->n);
   }
@@ -885,6 +994,8 @@ psp_status psp_factor_solve_batch(psp_handle h, const double* A_vals, const doub
   if (h->phase_events) {
     if ((s = phase_mark(h, h->sev, h->ns))) return s;
   }
+  h->last_solve = solve_launch(h).s_tmem ? PSP_KERNEL_BATCH_TMEM : PSP_KERNEL_BATCH;
+  h->last_solve_fwd = 0;
   CUDA_TRY(h, psp::launch_solve(h->plan, solve_launch(h), (const double*)h->V_d.p, b, h->n, 1,
                                 (double*)h->X_d.p, (double*)h->sscratch_d.p, h->K_pad, false,
                                 h->stream));
@@ -912,6 +1023,8 @@ psp_status psp_solve_batch(psp_handle h, int32_t R, const double* B, int64_t ldb
     if ((s = phase_mark(h, h->sev, h->ns))) return s;
   }
   if (use_coop(h, R)) {
+    h->last_solve = PSP_KERNEL_COOP;
+    h->last_solve_fwd = 1;
     CUDA_TRY(h, psp::launch_coop_solve(h->plan, h->coop, (const double*)h->V_d.p, B, ldb, R,
                                        (double*)h->X_d.p, h->K,
                                        kBlock / h->launch.f_groups * h->launch.f_lanes, h->stream));
@@ -922,6 +1035,8 @@ psp_status psp_solve_batch(psp_handle h, int32_t R, const double* B, int64_t ldb
     h->solved = true;
     return PSP_OK;
   }
+  h->last_solve = solve_launch(h, R).s_tmem ? PSP_KERNEL_BATCH_TMEM : PSP_KERNEL_BATCH;
+  h->last_solve_fwd = 1;
   CUDA_TRY(h, psp::launch_solve(h->plan, solve_launch(h, R), (const double*)h->V_d.p, B, ldb, R,
                                 (double*)h->X_d.p, (double*)h->sscratch_d.p, h->K_pad, true,
                                 h->stream));
@@ -1009,6 +1124,15 @@ psp_status psp_get_phase_times(psp_handle h, float* ms_h) {
     ms_h[q] = m >= 2 ? (float)(sum / (double)(m / 2)) : 0.f;
   }
   h->nf = h->ns = 0;
+  return PSP_OK;
+}
+
+psp_status psp_get_last_kernels(psp_handle h, int32_t* kernels_h) {
+  if (!h || !kernels_h) return PSP_ERR_ARG;
+  kernels_h[0] = h->last_factor;
+  kernels_h[1] = h->last_factor_aug;
+  kernels_h[2] = h->last_solve;
+  kernels_h[3] = h->last_solve_fwd;
   return PSP_OK;
 }
 
@@ -1134,6 +1258,9 @@ psp_status psp_get_perturbations(psp_handle h, double* eps_h) {
 psp_status psp_recover(psp_handle h, double* x) {
   if (!h || !x) return PSP_ERR_ARG;
   if (!h->solved || h->W == 0) return fail(h, PSP_ERR_STATE, "solve_batch and set_weights first");
+  // the batch-infeasible flag describes THIS combination (a re-perturbed, refactored batch
+  // must not inherit an earlier call's flag)
+  CUDA_TRY(h, cudaMemsetAsync(h->flag_d.p, 0, sizeof(int32_t), h->stream));
   if (h->w_uni) {
     CUDA_TRY(h, psp::launch_recover_uni(h->plan, h->W, h->R, h->w_uni, (const double*)h->wval_d.p,
                                         (const double*)h->X_d.p, (const int32_t*)h->status_d.p, x,

@@ -24,9 +24,12 @@ constexpr int kSolveMaxC = 16;        // records with c <= kSolveMaxC take the u
 constexpr int kMaxWarpsCta = 16;      // warps per CTA (all consumers: self-refilling ring)
 constexpr int kFusedMax = 12;         // pivots with c <= kFusedMax: u in registers, no scratch
 constexpr int kPairMax = 8;          // supernode pairs for c <= kPairMax
+constexpr int kSpillCap = 127;        // capacity-planned programs: pending slots per lane (+ the
+                                      // dummy = 128 slots = 256 TMEM columns, 2 CTAs per SM)
 
 // Record types of the programs (bits 28..31 of a record's first word).
-enum : uint32_t { kRecBirth = 1u, kRecPivot = 2u, kRecUpdate = 3u, kRecEnd = 4u, kRecYEnd = 5u };
+enum : uint32_t { kRecBirth = 1u, kRecPivot = 2u, kRecUpdate = 3u, kRecEnd = 4u, kRecYEnd = 5u,
+                  kRecSpill = 6u, kRecReload = 7u };
 
 // Device-side programs (see psp_plan.cpp for their meaning).
 struct DevicePlan {
@@ -41,6 +44,7 @@ struct DevicePlan {
   const int32_t* f_patch_pos = nullptr;
   const int32_t* f_patch_src = nullptr;
   int32_t f_aug = 0;                   // 1: program of [A | b] (y_p written to X)
+  int32_t f_gspill = 0;                // capacity-planned program: spill entries per lane
   // solve program: forward (ascending) records, YEND, backward (descending) records, END
   int32_t y_slots = 0, x_slots = 0, s_chunk_words = 0, s_nchunks = 0;
   const int32_t* s_stream = nullptr;
@@ -93,6 +97,7 @@ struct LaunchInfo {
   int f_ctas_per_sm = 0;
   int f_stages = 4;            // program ring stages of the factor (4 or 8)
   bool f_tmem = false;         // (1, 1, 1) with warps 0..3 holding their slots in TMEM
+  bool f_pair_lanes = false;   // compact TMEM kernel, 2 lanes (32-lane slabs) per thread
   int f_off_tscr = 0;          // TMEM warps' scratch rows (shared memory)
   // solve
   bool s_live_smem = false;
@@ -116,6 +121,7 @@ struct LaunchInfo {
 // variant, 2 = disable it.
 bool choose_launch(const DevicePlan& p, LaunchInfo& li, int force_groups, int force_warps,
                    int force_lanes, int force_slab_warps, int force_tmem, int force_solve_tmem);
+bool choose_launch_spill(const DevicePlan& p, LaunchInfo& li, int force_warps);
 cudaError_t configure_kernels(const DevicePlan& p, LaunchInfo& li, int force_groups,
                               int force_warps, int force_lanes, int force_slab_warps,
                               int force_tmem, int force_solve_tmem);
@@ -128,7 +134,7 @@ cudaError_t launch_pivot_tol(const DevicePlan& p, const double* A_vals, double* 
 cudaError_t launch_factor(const DevicePlan& p, const LaunchInfo& li, const int32_t* prog,
                           const double* eps, const double* tol_dev, double tol_value, double* V,
                           double* gscratch, double* gscr, int32_t* status, int32_t K_pad,
-                          double* Y, cudaStream_t stream);
+                          double* Y, double* gspill, cudaStream_t stream);
 // g_k = max|U| / max|A_k| per lane, from the factor in V (growth monitoring)
 cudaError_t launch_residual(int32_t n, const int32_t* row_ptr, const int32_t* col_idx,
                             const double* A, int32_t W, int32_t R, const double* B, const double* x,

@@ -425,9 +425,26 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
         }
       }
   }
-  std::vector<int32_t> fslot;
-  P.f_slots = colour(n, first, death, false, fslot);
-  const int32_t dummy_slot = P.f_slots++;   // target of the padding births (never read)
+  // all_slots (the capacity-planned programs): every operand a pending slot — an entry
+  // that no update touches is born (its value of A, + eps*d on the diagonal) at the pivot
+  // that consumes it and dies there, so the kernel reads operands with unconditional slot
+  // loads (no slot-or-immediate selection).  The arithmetic is the same: the birth's
+  // a_ii + (eps*d_i) is the pivot path's a_pp + (eps*d_p).
+  if (P.all_slots)
+    for (int32_t p = 0; p < n; ++p) {
+      auto mk = [&](int32_t e) {
+        if (first[e] < 0) {
+          first[e] = p;
+          death[e] = p;
+        }
+      };
+      mk(entry(p, p));
+      for (int32_t a : lcol[p]) {
+        mk(entry(a, p));
+        mk(entry(p, a));
+      }
+      if (aug) mk(entry_b(p));
+    }
   P.f_births = 0;
   // inverse entry -> (i, j) for births
   std::vector<int32_t> ent_i(n_ent), ent_j(n_ent);
@@ -448,6 +465,200 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
   std::vector<std::vector<int32_t>> births_at(n);
   for (int32_t e = 0; e < n_ent; ++e)
     if (first[e] >= 0) births_at[first[e]].push_back(e);
+  // Slot-store capacity (HostPlan::cap): the peak pending set of the unlimited plan
+  // (interval colouring) decides whether the capacity-planned program is needed.
+  std::vector<int32_t> fslot;
+  P.f_peak = colour(n, first, death, false, fslot);
+  bool capped = P.cap > 0 && P.f_peak > P.cap;
+  const int32_t C = P.cap;
+  // Per pivot: the pending entries of its update block (targets, + the right-hand side
+  // column) and the pending entries it consumes (pivot, L column, U row, y_p).  Disjoint:
+  // block entries have both indices > p, consumed ones one index = p.
+  auto block_of = [&](int32_t p, std::vector<int32_t>& u) {
+    const auto& L = lcol[p];
+    for (int32_t a : L) {
+      for (int32_t b : L) u.push_back(entry(a, b));
+      if (aug) u.push_back(entry_b(a));
+    }
+  };
+  auto consumed_of = [&](int32_t p, std::vector<int32_t>& u) {
+    auto add = [&](int32_t e) {
+      if (first[e] >= 0) u.push_back(e);
+    };
+    add(entry(p, p));
+    for (int32_t a : lcol[p]) {
+      add(entry(a, p));
+      add(entry(p, a));
+    }
+    if (aug) add(entry_b(p));
+  };
+  auto need_of = [&](int32_t p) {
+    std::vector<int32_t> u;
+    block_of(p, u);
+    consumed_of(p, u);
+    return (int32_t)u.size();
+  };
+  // Supernode pairs: pivot p and q = p + 1 with L(:, p) = {q} u L(:, q) (a fundamental
+  // supernode link, q the etree parent of p) share one record: q's update block is the
+  // trailing part of p's, so the kernel applies both updates to it with one load/store
+  // (in the canonical order: p's, then q's).  Entries first touched at q: none.  With a
+  // capacity, only pairs whose step fits it.
+  std::vector<char> paired(n, 0);
+  P.f_pairs = 0;
+  if (P.fuse_pairs)
+    for (int32_t p = 0; p + 1 < n; ++p) {
+      const auto& Lp = lcol[p];
+      const auto& Lq = lcol[p + 1];
+      if (Lp.empty() || Lp[0] != p + 1 || (int32_t)Lp.size() + (aug ? 1 : 0) > kPairMax) continue;
+      if (Lp.size() != Lq.size() + 1 || !std::equal(Lq.begin(), Lq.end(), Lp.begin() + 1)) continue;
+      if (!births_at[p + 1].empty()) continue;
+      if (capped && need_of(p) > C) continue;
+      paired[p] = 1;
+      ++P.f_pairs;
+      ++p;   // q is not the first of another pair
+    }
+  // Steps = the record groups the kernel executes in order: one per pivot or pair.  With
+  // a capacity, a pivot whose block + consumed entries exceed it is SPLIT into step A
+  // (pivot record: L column and U row read into scratch, consumed entries die) and step B
+  // (its births in BIRTH records, then UPDATE records): the large-pivot path.
+  std::vector<int32_t> stepA(n, -1), stepB(n, -1);
+  std::vector<char> split(n, 0);
+  int32_t n_steps = 0;
+  for (int32_t p = 0; p < n; ++p) {
+    split[p] = capped && !paired[p] && need_of(p) > C;
+    stepA[p] = n_steps++;
+    stepB[p] = split[p] ? n_steps++ : stepA[p];
+    if (paired[p]) {
+      stepA[p + 1] = stepB[p + 1] = stepA[p];
+      ++p;
+    }
+  }
+  P.c_scr_need = 0;
+  for (int32_t p = 0; p < n; ++p) {
+    const int32_t cu = (int32_t)lcol[p].size() + (aug ? 1 : 0);
+    if (split[p] || cu > kFusedMax) P.c_scr_need = std::max(P.c_scr_need, cu);
+  }
+  // capped: per entry its (from step, slot) residency intervals; spill / reload ops per step
+  std::vector<std::vector<std::pair<int32_t, int32_t>>> slot_hist;
+  std::vector<std::vector<std::pair<int32_t, int32_t>>> spill_at, reload_at;   // (slot, gidx)
+  P.f_gspill = P.f_spills = P.f_reloads = 0;
+  if (capped) {
+    std::vector<std::vector<int32_t>> uses(n_steps);
+    for (int32_t p = 0; p < n; ++p) {
+      if (p > 0 && paired[p - 1] && stepA[p] == stepA[p - 1]) continue;   // q of a pair
+      consumed_of(p, uses[stepA[p]]);
+      block_of(p, uses[stepB[p]]);
+    }
+    for (auto& u : uses) {
+      std::sort(u.begin(), u.end());
+      u.erase(std::unique(u.begin(), u.end()), u.end());
+    }
+    std::vector<std::vector<int32_t>> use_steps(n_ent);
+    for (int32_t st = 0; st < n_steps; ++st)
+      for (int32_t e : uses[st]) use_steps[e].push_back(st);
+    std::vector<int32_t> where(n_ent, -1), gwhere(n_ent, -1), nxt(n_ent, 0), mark(n_ent, -1);
+    slot_hist.assign(n_ent, {});
+    spill_at.assign(n_steps, {});
+    reload_at.assign(n_steps, {});
+    std::vector<int32_t> free_slot, free_g, resident;
+    for (int32_t k = C - 1; k >= 0; --k) free_slot.push_back(k);
+    int32_t next_g = 0;
+    for (int32_t st = 0; st < n_steps && capped; ++st) {
+      const auto& N = uses[st];
+      for (int32_t e : N) mark[e] = st;
+      int32_t need = 0;
+      for (int32_t e : N) need += where[e] < 0;
+      const int32_t over = (int32_t)resident.size() + need - C;
+      if (over > 0) {   // Belady: evict the residents (not used now) with the furthest next use
+        std::vector<std::pair<int32_t, int32_t>> cand;   // (-next use, entry)
+        for (int32_t e : resident)
+          if (mark[e] != st) cand.push_back({-use_steps[e][nxt[e]], e});
+        if ((int32_t)cand.size() < over) {   // one step alone needs more than C slots:
+          capped = false;                       // no capped plan (unlimited slots instead)
+          break;
+        }
+        std::partial_sort(cand.begin(), cand.begin() + over, cand.end());
+        for (int32_t k = 0; k < over; ++k) {
+          const int32_t e = cand[k].second;
+          int32_t g;
+          if (!free_g.empty()) {
+            g = free_g.back();
+            free_g.pop_back();
+          } else {
+            g = next_g++;
+          }
+          spill_at[st].push_back({where[e], g});
+          free_slot.push_back(where[e]);
+          where[e] = -1;
+          gwhere[e] = g;
+          ++P.f_spills;
+        }
+        resident.erase(std::remove_if(resident.begin(), resident.end(),
+                                      [&](int32_t e) { return where[e] < 0; }),
+                       resident.end());
+      }
+      for (int32_t e : N) {
+        if (where[e] >= 0) continue;
+        const int32_t sl = free_slot.back();
+        free_slot.pop_back();
+        if (gwhere[e] >= 0) {   // spilled: reload before this step
+          reload_at[st].push_back({sl, gwhere[e]});
+          free_g.push_back(gwhere[e]);
+          gwhere[e] = -1;
+          ++P.f_reloads;
+        }
+        where[e] = sl;
+        slot_hist[e].push_back({st, sl});
+        resident.push_back(e);
+      }
+      for (int32_t e : N) ++nxt[e];
+      bool died = false;
+      for (int32_t e : N)
+        if (stepA[death[e]] == st) {   // consumed at its death pivot's (first) step
+          free_slot.push_back(where[e]);
+          where[e] = -1;
+          died = true;
+        }
+      if (died)
+        resident.erase(std::remove_if(resident.begin(), resident.end(),
+                                      [&](int32_t e) { return where[e] < 0; }),
+                       resident.end());
+    }
+    P.f_gspill = next_g;
+  }
+  if (capped) {
+    P.f_slots = C;
+  } else {   // unlimited slots: interval colouring (no split steps are needed then)
+    slot_hist.clear();
+    spill_at.clear();
+    reload_at.clear();
+    P.f_gspill = P.f_spills = P.f_reloads = 0;
+    P.f_slots = P.f_peak;
+    if (P.cap > 0 && P.f_peak > P.cap) P.f_peak = -P.f_peak;   // (capacity infeasible)
+    for (int32_t p = 0; p < n; ++p) {
+      if (split[p]) {
+        split[p] = 0;
+        stepB[p] = stepA[p];
+      }
+    }
+  }
+  const int32_t dummy_slot = P.f_slots++;   // target of the padding births (never read)
+  const int32_t dummy_g = P.f_gspill;       // spill-area entry of the padding spill ops
+  if (capped) ++P.f_gspill;
+  int32_t cur_step = 0;
+  auto slot_of = [&](int32_t e) -> int32_t {
+    if (!capped) return fslot[e];
+    const auto& hst = slot_hist[e];
+    for (int32_t k = (int32_t)hst.size() - 1; k >= 0; --k)
+      if (hst[k].first <= cur_step) return hst[k].second;
+    return dummy_slot;   // (unreachable: every used entry has a residency at its step)
+  };
+  // Self-check of the slot plan while the records are emitted, in kernel execution order:
+  // slot / spill-entry contents are simulated (births, spills, reloads), and every slot a
+  // record reads (operands, update targets) must hold the entry the record means.
+  std::vector<int32_t> sim_slot(P.f_slots + 1, -1), sim_g(P.f_gspill + 1, -1);
+  std::vector<std::pair<int32_t, int32_t>> checks;   // (slot, entry) read by the current record
+  P.plan_ok = true;
   // Factor stream (v4): one record per pivot, 16-byte aligned, packed into fixed-size
   // chunks that the kernel pulls into a CTA-shared ring with bulk async copies.  Values
   // of A and d are IMMEDIATES: 64-bit cells patched into a device copy of the stream
@@ -459,17 +670,22 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
   //          + nbd diagonal births  [slot, 0, a_ii (2), d_i (2), 0, 0]: a_ii + eps*d_i
   //          + nba births           [slot, 0, a_ij (2)] (structural zeros: a_ij = 0);
   //            nba is a multiple of 4 (padding births write a dummy slot never read)
-  //          + c L operands, c U operands (4 words each)
+  //          + c L operands, cu U operands (4 words each; cu = c (+ 1: y_p of [A | b]),
+  //            padded to a multiple of 4 with immediate zeros)
   //          + (flags & 2 == 0) c rows x ws target slots of the c x c update block
   //          flags: 1 = the pivot was never updated (add eps*d_p); 2 = c > kFusedMax,
   //          the update comes in UPDATE records; 4 = supernode pair: the record also
   //          carries pivot q = p + 1 (row 0 of the block is q's row, column 0 its column);
-  //          ws = row stride (8 * ceil(c / 8))
+  //          ws = row stride (8 * ceil(cu / 8)); padding columns hold the dummy slot
   //   BIRTH  [1<<28, 0, nbd, nba, 0, 0, 0, 0] + births: those of the next pivot that do
   //          not fit its record
   //   UPDATE [3<<28 | c, a0, na, ws, 0, 0, 0, 0] + na rows x ws target slots (rows
   //          a0 .. a0+na-1 of a pivot with c > kFusedMax)
   //   END    [4<<28, ...]
+  //   SPILL  [6<<28 | cnt, 0, 0, 0] + cnt x [slot, gidx]: slot -> the lane's spill entry gidx
+  //   RELOAD [7<<28 | cnt, 0, 0, 0] + cnt x [slot, gidx]: spill entry gidx -> slot
+  //          (capacity-planned programs only; before the BIRTH/PIVOT records of a step:
+  //          the evictions that make room for the step, then its reloads)
   // Births of pivot p are the entries first touched by p's update; the pivot's output
   // position (lofs[p], dofs[p]) is implicit: pivots come in order.
   constexpr size_t kMaxRec = 508;   // words: records stay within one 2 KB chunk
@@ -481,6 +697,10 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
     while (r.size() % 4) r.push_back(0);
   };
   auto push = [&](std::vector<int32_t>&& r, std::vector<std::pair<int32_t, int32_t>>&& pt) {
+    for (const auto& ck : checks)
+      if (ck.first < 0 || ck.first >= (int32_t)sim_slot.size() || sim_slot[ck.first] != ck.second)
+        P.plan_ok = false;
+    checks.clear();
     pad4(r);
     max_rec = std::max(max_rec, r.size());
     recs.push_back(std::move(r));
@@ -502,7 +722,8 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
                      int32_t i, int32_t j) {
     const int32_t e = j == n ? entry_b(i) : entry(i, j);
     if (first[e] >= 0) {
-      r.insert(r.end(), {fslot[e], 0, 0, 0});
+      checks.push_back({slot_of(e), e});
+      r.insert(r.end(), {slot_of(e), 0, 0, 0});
     } else {
       r.insert(r.end(), {-1, 0});
       imm(r, pt, a_src(i, j));
@@ -510,7 +731,8 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
   };
   auto birth = [&](std::vector<int32_t>& r, std::vector<std::pair<int32_t, int32_t>>& pt, int32_t e) {
     const int32_t i = ent_i[e], j = ent_j[e];
-    r.insert(r.end(), {fslot[e], 0});
+    r.insert(r.end(), {slot_of(e), 0});
+    sim_slot[slot_of(e)] = e;
     imm(r, pt, a_src(i, j));
     if (i == j) {
       imm(r, pt, -1 - i);
@@ -520,35 +742,33 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
   };
   P.adiag.assign(n, -1);
   for (int32_t i = 0; i < n; ++i) P.adiag[i] = a_index(i, i);
-  // Supernode pairs: pivot p and q = p + 1 with L(:, p) = {q} u L(:, q) (a fundamental
-  // supernode link, q the etree parent of p) share one record: q's update block is the
-  // trailing part of p's, so the kernel applies both updates to it with one load/store
-  // (in the canonical order: p's, then q's).  Entries first touched at q: none.
-  std::vector<char> paired(n, 0);
-  P.f_pairs = 0;
-  if (P.fuse_pairs)
-    for (int32_t p = 0; p + 1 < n; ++p) {
-      const auto& Lp = lcol[p];
-      const auto& Lq = lcol[p + 1];
-      if (Lp.empty() || Lp[0] != p + 1 || (int32_t)Lp.size() + (aug ? 1 : 0) > kPairMax) continue;
-      if (Lp.size() != Lq.size() + 1 || !std::equal(Lq.begin(), Lq.end(), Lp.begin() + 1)) continue;
-      if (!births_at[p + 1].empty()) continue;
-      paired[p] = 1;
-      ++P.f_pairs;
-      ++p;   // q is not the first of another pair
+  // SPILL / RELOAD  [type<<28 | cnt, 0, 0, 0] + cnt x [slot, gidx] (cnt a multiple of 4:
+  // padding ops move the dummy slot to / from the dummy spill entry)
+  auto emit_moves = [&](uint32_t type, const std::vector<std::pair<int32_t, int32_t>>& ops) {
+    constexpr size_t kPer = (kMaxRec - 4) / 2 / 4 * 4;
+    for (size_t o0 = 0; o0 < ops.size(); o0 += kPer) {
+      const size_t o1 = std::min(ops.size(), o0 + kPer);
+      size_t cnt = o1 - o0;
+      const size_t cnt4 = (cnt + 3) & ~(size_t)3;
+      std::vector<int32_t> r = {(int32_t)((type << 28) | (uint32_t)cnt4), 0, 0, 0};
+      for (size_t o = o0; o < o1; ++o) {
+        r.insert(r.end(), {ops[o].first, ops[o].second});
+        if (type == kRecSpill) {
+          sim_g[ops[o].second] = sim_slot[ops[o].first];
+          sim_slot[ops[o].first] = -1;
+        } else {
+          sim_slot[ops[o].first] = sim_g[ops[o].second];
+        }
+      }
+      for (; cnt < cnt4; ++cnt) r.insert(r.end(), {dummy_slot, dummy_g});
+      push(std::move(r), {});
     }
-  for (int32_t p = 0; p < n; ++p) {
-    const auto& L = lcol[p];
-    const int32_t c = (int32_t)L.size();
-    const int32_t cu = c + (aug ? 1 : 0);   // U-row columns (+ the right-hand side)
-    const int32_t ws = 8 * ((cu + 7) / 8);
-    const bool fused = cu <= kFusedMax;
-    std::vector<int32_t> bd, bo;   // diagonal / other births (entry ids)
-    for (int32_t e : births_at[p]) (ent_i[e] == ent_j[e] ? bd : bo).push_back(e);
-    const size_t fixed = 8 + 4 + 12 + 4 * (size_t)(c + cu) + (fused ? (size_t)c * ws : 0);
-    // births that do not fit the pivot's record go first, in BIRTH records
-    size_t qd = 0, qo = 0;
-    while (fixed + 8 * (bd.size() - qd) + 4 * (bo.size() - qo) > kMaxRec &&
+  };
+  // births in BIRTH records (those that do not fit a pivot's record, or all of a split
+  // pivot's, emitted after its PIVOT record)
+  auto birth_records = [&](const std::vector<int32_t>& bd, const std::vector<int32_t>& bo, size_t& qd,
+                           size_t& qo, size_t budget) {
+    while (budget + 8 * (bd.size() - qd) + 4 * (bo.size() - qo) > kMaxRec &&
            (qd < bd.size() || qo < bo.size())) {
       std::vector<int32_t> b = {(int32_t)(kRecBirth << 28), 0, 0, 0, 0, 0, 0, 0};
       std::vector<std::pair<int32_t, int32_t>> pt;
@@ -560,6 +780,35 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
       b[3] = no;
       push(std::move(b), std::move(pt));
     }
+  };
+  for (int32_t p = 0; p < n; ++p) {
+    cur_step = stepA[p];
+    if (capped) {
+      emit_moves(kRecSpill, spill_at[cur_step]);
+      emit_moves(kRecReload, reload_at[cur_step]);
+    }
+    const auto& L = lcol[p];
+    const int32_t c = (int32_t)L.size();
+    const int32_t cu = c + (aug ? 1 : 0);   // U-row columns (+ the right-hand side)
+    const int32_t ws = 8 * ((cu + 7) / 8);
+    const bool sp = split[p];
+    const bool fused = cu <= kFusedMax && !sp;
+    std::vector<int32_t> bd, bo;   // diagonal / other births (entry ids)
+    for (int32_t e : births_at[p]) (ent_i[e] == ent_j[e] ? bd : bo).push_back(e);
+    const int32_t cu4 = (cu + 3) & ~3;   // U operands padded to a multiple of 4 (immediate 0)
+    const size_t fixed = 8 + 4 + 12 + 4 * (size_t)(c + cu4) + (fused ? (size_t)c * ws : 0);
+    size_t qd = 0, qo = 0;
+    std::vector<int32_t> bdB, boB;   // split pivot: the block's births (step B)
+    if (sp) {   // the operands born at p (all_slots) stay in the pivot record (step A)
+      auto part = [&](std::vector<int32_t>& v, std::vector<int32_t>& vb) {
+        std::vector<int32_t> keep;
+        for (int32_t e : v) (death[e] == p ? keep : vb).push_back(e);
+        v.swap(keep);
+      };
+      part(bd, bdB);
+      part(bo, boB);
+    }
+    birth_records(bd, bo, qd, qo, fixed);   // births that do not fit the record go first
     const int32_t e_pp = entry(p, p);
     const int32_t flags = (first[e_pp] < 0 ? 1 : 0) | (fused ? 0 : 2) | (paired[p] ? 4 : 0);
     const int32_t nbo = (int32_t)(bo.size() - qo), nbo4 = (nbo + 3) & ~3;
@@ -574,15 +823,41 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
     for (int32_t k = 0; k < c; ++k) operand(r, pt, L[k], p);
     for (int32_t k = 0; k < c; ++k) operand(r, pt, p, L[k]);
     if (aug) operand(r, pt, p, n);   // y_p
+    for (int32_t k = cu; k < cu4; ++k)   // (all_slots: the dummy slot, else an immediate 0)
+      r.insert(r.end(), {P.all_slots ? dummy_slot : -1, 0, 0, 0});
     auto row = [&](std::vector<int32_t>& out, int32_t a) {
       for (int32_t b = 0; b < ws; ++b)
-        out.push_back(b < c ? fslot[entry(L[a], L[b])] : (b < cu ? fslot[entry_b(L[a])] : 0));
+        if (b < cu) {
+          const int32_t e = b < c ? entry(L[a], L[b]) : entry_b(L[a]);
+          checks.push_back({slot_of(e), e});
+          out.push_back(slot_of(e));
+        } else {
+          out.push_back(dummy_slot);   // padding columns: the dummy slot (never read)
+        }
     };
     if (fused)
       for (int32_t a = 0; a < c; ++a) row(r, a);
     push(std::move(r), std::move(pt));
     if (paired[p]) ++p;   // q's work is in p's record
     if (!fused) {
+      if (sp) {   // step B: make room, reload, births, then the update rows
+        cur_step = stepB[p];
+        emit_moves(kRecSpill, spill_at[cur_step]);
+        emit_moves(kRecReload, reload_at[cur_step]);
+        size_t zd = 0, zo = 0;
+        birth_records(bdB, boB, zd, zo, 20);
+        if (zd < bdB.size() || zo < boB.size()) {   // the rest (fits one record)
+          std::vector<int32_t> b = {(int32_t)(kRecBirth << 28), 0, 0, 0, 0, 0, 0, 0};
+          std::vector<std::pair<int32_t, int32_t>> pt2;
+          int32_t nd = 0, no = 0;
+          while (zd < bdB.size()) birth(b, pt2, bdB[zd++]), ++nd;
+          while (zo < boB.size()) birth(b, pt2, boB[zo++]), ++no;
+          while (no % 4) b.insert(b.end(), {dummy_slot, 0, 0, 0}), ++no;
+          b[2] = nd;
+          b[3] = no;
+          push(std::move(b), std::move(pt2));
+        }
+      }
       const int32_t rows_per = std::max<int32_t>(1, (int32_t)((kMaxRec - 8) / ws));
       for (int32_t a0 = 0; a0 < c; a0 += rows_per) {
         const int32_t na = std::min(rows_per, c - a0);

@@ -28,6 +28,20 @@ struct HostPlan {
   // side, never a pivot): every U row gets u_{p b} = y_p, the forward-substitution
   // result, which the factor kernel writes to X instead of the DU region
   bool aug = false;
+  // input: capacity of the pending-slot store per lane (0 = unlimited: one slot per
+  // simultaneously pending entry, interval colouring).  With a capacity below the peak
+  // pending set, the entries with the furthest next use are spilled to a per-lane global
+  // area (SPILL records) and reloaded before their next use (RELOAD records): Belady's
+  // rule over the record steps.  f_slots is then cap + 1 (the dummy slot), f_gspill the
+  // spill-area entries per lane, f_spills / f_reloads the operation counts per lane.
+  int32_t cap = 0;
+  // input: every operand a pending slot (operands no update touches are born at their
+  // pivot): unconditional slot loads in the kernel (the capacity-planned programs)
+  bool all_slots = false;
+  int32_t f_gspill = 0, f_spills = 0, f_reloads = 0, f_peak = 0;
+  bool plan_ok = true;             // output: the emitted program passed the slot self-check
+  int32_t c_scr_need = 0;          // output: scratch rows of the large-pivot path (max c + aug
+                                   // over pivots with c > kFusedMax or split steps)
   std::vector<int32_t> f_stream;
   // immediates of the factor stream: word position of each 64-bit cell and its source
   // (>= 0: A index, nnz_A = structural zero, nnz_A + 1 + i: b[i] (original numbering);

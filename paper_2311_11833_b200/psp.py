@@ -26,9 +26,11 @@ EXPORTS = ["psp_create", "psp_destroy", "psp_set_stream", "psp_status_string",
            "psp_get_solutions", "psp_get_phase_times", "psp_get_lane_growth", "psp_estimate_rho",
            "psp_set_weights", "psp_recover", "psp_get_lane_status", "psp_solve_host", "psp_solve_host_async",
            "psp_synchronize", "psp_ladder_weights", "psp_set_option", "psp_get_factor", "psp_residual",
-           "psp_rescale_failed_rows", "psp_get_perturbations"]
+           "psp_rescale_failed_rows", "psp_get_perturbations", "psp_get_last_kernels"]
+KERNEL = {0: "none", 1: "coop", 2: "batch", 3: "batch_tmem", 4: "batch_spill"}
 OPT = {"factor_groups": 1, "factor_warps": 2, "factor_lanes": 3, "factor_slab_warps": 4,
-       "factor_pairs": 5, "factor_tmem": 6, "solve_tmem": 7, "phase_events": 8, "growth": 9, "coop": 10}
+       "factor_pairs": 5, "factor_tmem": 6, "solve_tmem": 7, "phase_events": 8, "growth": 9, "coop": 10,
+       "factor_spill": 11}
 
 
 class SymbolicInfo(ctypes.Structure):
@@ -42,7 +44,10 @@ class SymbolicInfo(ctypes.Structure):
                 ("factor_warps_per_cta", ctypes.c_int32), ("factor_pend_smem", ctypes.c_int32),
                 ("solve_live_smem", ctypes.c_int32), ("aug_ok", ctypes.c_int32),
                 ("aug_max_live", ctypes.c_int32), ("aug_warps_per_cta", ctypes.c_int32),
-                ("aug_pend_smem", ctypes.c_int32)]
+                ("aug_pend_smem", ctypes.c_int32), ("spill_ok", ctypes.c_int32),
+                ("spill_cap", ctypes.c_int32), ("spill_ops", ctypes.c_int32),
+                ("spill_entries", ctypes.c_int32), ("aug_spill_ops", ctypes.c_int32),
+                ("spill_warps_per_cta", ctypes.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -91,6 +96,7 @@ def lib():
             "psp_ladder_weights": [I32, P, P, P],
             "psp_set_option": [P, I32, I64],
             "psp_get_factor": [P, I32, P],
+            "psp_get_last_kernels": [P, P],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -257,6 +263,13 @@ class Solver:
         ms = (ctypes.c_float * 2)()
         self._check(lib().psp_get_phase_times(self.h, ms))
         return float(ms[0]), float(ms[1])
+
+    def psp_get_last_kernels(self):
+        """(factor kernel, factor fused forward?, solve kernel, solve ran forward?) of the
+        last numeric calls; kernel names from KERNEL (psp.h PSP_KERNEL_*)."""
+        k = np.zeros(4, dtype=np.int32)
+        self._check(lib().psp_get_last_kernels(self.h, _np_ptr(k)))
+        return KERNEL[int(k[0])], bool(k[1]), KERNEL[int(k[2])], bool(k[3])
 
     def psp_get_solutions(self, out=None):
         out = out if out is not None else self.torch.empty((self.K, self.R, self.n), dtype=self.torch.float64,

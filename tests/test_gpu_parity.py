@@ -24,8 +24,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def gpu_run(s, eps, ordering_kind="mindeg", first=-1, tol=0.0, B=None, ladders=None,
-            w_csr=None, lanes_out=True):
+            w_csr=None, lanes_out=True, coop=None):
     solver = psp.Solver(0)
+    if coop is not None:
+        solver.psp_set_option("coop", coop)
     solver.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering=ordering_kind, first_node=first)
     info, perm = solver.psp_get_symbolic_info()
     # the oracle's own elimination order (never the product's): integer parity
@@ -324,16 +326,43 @@ def test_values_only_refactorisation_many_jacobians(coop):
     solver.close()
 
 
-def test_default_pivot_tol_and_lane_independence():
+@pytest.mark.parametrize("coop", [0, 2])
+def test_default_pivot_tol_and_lane_independence(coop):
     w = config(1)
     s = w.system()
     eps = w.eps()
-    g1 = gpu_run(s, eps)                       # pivot_tol <= 0: device-computed default
+    g1 = gpu_run(s, eps, coop=coop)            # pivot_tol <= 0: device-computed default
+    assert g1["solver"].psp_get_last_kernels()[0] == ("coop" if coop == 0 else
+                                                      g1["solver"].psp_get_last_kernels()[0])
+    if coop == 2:
+        assert g1["solver"].psp_get_last_kernels()[0] != "coop"
     # the same lanes at other batch positions (another slab, another warp lane)
     eps2 = np.r_[np.full(45, 3e-3), eps[::-1]]
-    g2 = gpu_run(s, eps2)
+    g2 = gpu_run(s, eps2, coop=coop)
     assert np.array_equal(g2["X"][45:][::-1], g1["X"])
     assert (g1["status"] == 0).all()
+    Xo, sto = oracle.dense_batch(s, g1["operm"], eps, oracle.default_tol(s.n, s.row_ptr, s.col_idx, s.vals))
+    assert np.array_equal(g1["X"], Xo) and np.array_equal(g1["status"], sto)
+
+
+@pytest.mark.parametrize("coop", [0, 2])
+def test_default_pivot_tol_discriminating_pivot(coop):
+    """The device's default tolerance (n u ||A||_1, R10) decides a pivot the same way as
+    oracle.default_tol where it matters: a lane whose leading pivot eps_k d_p (the
+    structurally zero diagonal of the leading-zero order) sits just below tol
+    fails at step 0, one just above succeeds (tol/2 and 2 tol; both sides exact)."""
+    w = config(1)
+    s = w.system()
+    tol = oracle.default_tol(s.n, s.row_ptr, s.col_idx, s.vals)
+    dp = s.d[s.slot_p]
+    e_lo, e_hi = 0.5 * tol / abs(dp), 2.0 * tol / abs(dp)
+    eps = np.r_[w.eps(), e_lo, -e_lo, e_hi, -e_hi]
+    g = gpu_run(s, eps, "mindeg_first", s.slot_p, 0.0, coop=coop)   # 0.0: the device default
+    Xo, sto = oracle.SparseOracle(s, g["operm"]).batch(eps, tol)
+    assert np.array_equal(g["status"], sto)
+    assert list(sto[-4:-2]) == [1, 1] and (sto[-2:] != 1).all() and (sto[:-4] == 0).all()
+    ok = sto == 0
+    assert np.array_equal(g["X"][ok], Xo[ok])
 
 
 def test_host_api_e2e_matches_device_path():
@@ -481,6 +510,7 @@ def test_factor_kernel_variants_bitwise(gjp):
     K = 100
     eps = rng.choice([-1, 1], K) * 10.0 ** rng.uniform(-6, -2, K)
     solver = psp.Solver(0)
+    solver.psp_set_option("coop", 2)          # K = 100 would otherwise take the coop kernels
     solver.psp_set_option("factor_groups", G)
     solver.psp_set_option("factor_lanes", J)
     solver.psp_set_option("factor_slab_warps", P)
@@ -490,12 +520,15 @@ def test_factor_kernel_variants_bitwise(gjp):
     assert (info["factor_groups"], info["factor_lanes_per_thread"], info["factor_slab_warps"]) == gjp
     solver.psp_set_perturbations(eps, s.d)
     solver.psp_factor_batch(torch.tensor(s.vals, dtype=torch.float64, device="cuda"), 1e-300)
+    assert solver.psp_get_last_kernels()[0] in ("batch", "batch_tmem")
     solver.psp_solve_batch(torch.tensor(s.b.T.copy(), dtype=torch.float64, device="cuda"))
+    assert solver.psp_get_last_kernels()[2] in ("batch", "batch_tmem")
     X = solver.psp_get_solutions().cpu().numpy()
     Xo, sto = oracle.SparseOracle(s, perm).batch(eps, 1e-300)
     assert np.array_equal(X, Xo)
     # the factor itself, entry by entry, against a G=J=P=1 run
     ref = psp.Solver(0)
+    ref.psp_set_option("coop", 2)
     ref.psp_set_option("factor_groups", 1)
     ref.psp_set_option("factor_pairs", 1 - pairs if gjp == (1, 1, 1) else 1)
     ref.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering="mindeg_first", first_node=s.slot_p)
@@ -518,6 +551,7 @@ def test_factor_tmem_variant_bitwise(K):
     out = {}
     for tm in (1, 2):
         solver = psp.Solver(0)
+        solver.psp_set_option("coop", 2)      # (K <= 8 x SMs would take the coop kernels)
         solver.psp_set_option("factor_tmem", tm)
         solver.psp_set_option("solve_tmem", tm)
         solver.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering="mindeg")
@@ -527,6 +561,8 @@ def test_factor_tmem_variant_bitwise(K):
         solver.psp_set_perturbations(eps, s.d)
         solver.psp_factor_batch(torch.tensor(s.vals, dtype=torch.float64, device="cuda"), 1e-300)
         solver.psp_solve_batch(torch.tensor(s.b.T.copy(), dtype=torch.float64, device="cuda"))
+        want = "batch_tmem" if tm == 1 else "batch"
+        assert solver.psp_get_last_kernels() == (want, False, want, True)
         out[tm] = (solver, info, perm, solver.psp_get_solutions().cpu().numpy())
     solver, info, perm, X = out[1]
     Xo, sto = oracle.SparseOracle(s, perm).batch(eps, 1e-300)
@@ -550,11 +586,15 @@ def test_fused_factor_solve_bitwise(ci, K):
     outs = []
     for fused in (True, False):
         solver = psp.Solver(0)
+        solver.psp_set_option("coop", 2)      # (K <= 8 x SMs would take the coop kernels)
         solver.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering="mindeg")
         info, perm = solver.psp_get_symbolic_info()
         solver.psp_set_perturbations(eps, s.d)
         if fused:
             solver.psp_factor_solve_batch(A, b, 0.0)
+            kf, aug, ks, fwd = solver.psp_get_last_kernels()
+            assert kf in ("batch", "batch_tmem", "batch_spill") and ks in ("batch", "batch_tmem")
+            assert (aug, fwd) == ((True, False) if info["aug_ok"] == 2 else (False, True))
         else:
             solver.psp_factor_batch(A, 0.0)
             solver.psp_solve_batch(b.view(1, -1))
@@ -846,3 +886,99 @@ def test_sharded_recover_partials_sum_to_full():
     tot = run(0, cut) + run(cut, K)
     scale = np.abs(full).max()
     assert np.max(np.abs(tot - full)) <= 64 * np.finfo(float).eps * scale
+
+
+@pytest.mark.parametrize("K,fused", [(1000, False), (1000, True), (4133, True), (33, True)])
+def test_spill_factor_bitwise(K, fused):
+    """The capacity-planned factor (PSP_OPT_FACTOR_SPILL: <= 127 pending slots per lane,
+    the entries with the furthest next use spilled to a global area and reloaded before
+    their next use; 2 CTAs x 7 warps per SM) against the oracle and, factor entry by entry,
+    against the unlimited-slot TMEM kernel: ragged K, several CTAs, the fused [A | b]
+    program (its root step split into pivot and update steps) and the plain one."""
+    s = config(1).system()
+    rng = np.random.default_rng(K + 3)
+    eps = rng.choice([-1, 1], K) * 10.0 ** rng.uniform(-6, -2, K)
+    A = torch.tensor(s.vals, dtype=torch.float64, device="cuda")
+    b = torch.tensor(s.b[:, 0].copy(), dtype=torch.float64, device="cuda")
+    out = {}
+    for sp in (1, 2):
+        solver = psp.Solver(0)
+        solver.psp_set_option("coop", 2)
+        solver.psp_set_option("factor_spill", sp)
+        solver.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering="mindeg")
+        info, perm = solver.psp_get_symbolic_info()
+        if sp == 1:
+            assert info["spill_ok"] == 3 and info["spill_ops"] > 0 and info["aug_spill_ops"] > 0
+        solver.psp_set_perturbations(eps, s.d)
+        if fused:
+            solver.psp_factor_solve_batch(A, b, 0.0)
+        else:
+            solver.psp_factor_batch(A, 0.0)
+            solver.psp_solve_batch(b.view(1, -1))
+        kf, aug, ks, fwd = solver.psp_get_last_kernels()
+        assert kf == ("batch_spill" if sp == 1 else "batch_tmem")
+        assert aug == fused and fwd == (not fused)
+        rc, st = solver.psp_get_lane_status()
+        X = solver.psp_get_solutions().cpu().numpy()
+        F = [solver.psp_get_factor(k, info["nnz_LU"]) for k in sorted({0, 31, 32, K // 2, K - 1})]
+        out[sp] = (X, st, F, perm)
+    X, st, F, perm = out[1]
+    tol = oracle.default_tol(s.n, s.row_ptr, s.col_idx, s.vals)
+    sample = np.unique(np.r_[0, 1, 31, 32, 223, 224, K // 2, K - 2, K - 1]) if K > 300 else np.arange(K)
+    sample = sample[sample < K]
+    Xo, sto = oracle.SparseOracle(s, perm).batch(eps[sample], tol, B=s.b[:, :1])
+    assert np.array_equal(st[sample], sto)
+    ok = sto == 0
+    assert np.array_equal(X[sample][ok], Xo[ok])
+    assert np.array_equal(X, out[2][0]) and np.array_equal(st, out[2][1])
+    assert all(np.array_equal(f1, f2) for f1, f2 in zip(F, out[2][2]))
+
+
+def _bound_check(xh, xs, e_pred, X, Xp, wrow):
+    """Tolerance policy 3: ||x_hat - x*|| <= 1.5 ||e_pred|| + floor, floor =
+    10 sum_k |w_k| ||x_k - x_k^piv||; where e_pred dominates the floor, x* - x_hat = e_pred
+    vector-wise to within half its norm.  Per right-hand side."""
+    for r in range(xs.shape[0]):
+        floor = 10.0 * sum(abs(wk) * np.linalg.norm(X[k, r] - Xp[k, r]) for k, wk in wrow.items())
+        err = xs[r] - xh[r]
+        ne = np.linalg.norm(e_pred[r])
+        assert np.linalg.norm(err) <= 1.5 * ne + floor, (np.linalg.norm(err), ne, floor)
+        if ne > 100 * floor:
+            assert np.linalg.norm(err - e_pred[r]) <= 0.5 * ne + floor
+
+
+@pytest.mark.parametrize("m,base", [(1, 2e-3), (2, 2e-3), (2, 1e-2), (3, 2e-3), (4, 2e-3)])
+def test_recovered_vs_pivoted_within_predicted_error(m, base):
+    """The north star's third bar: the GPU's recovered x against the partial-pivot x*
+    within the truncation error Theorem 1 predicts for this ladder (its exact form (I3),
+    oracle.predicted_error), on the 300-bus Jacobian, the paper's alpha = 1..m ladder."""
+    w = config(1)
+    s = w.system()
+    mags = [base * j for j in range(1, m + 1)]
+    eps = ladder_eps(mags)
+    g = gpu_run(s, eps, ladders=[mags])
+    assert (g["status"] == 0).all()
+    xs, st = oracle.reference_solve(s)
+    assert st == 0
+    e_pred = oracle.predicted_error(s, mags)
+    Xp = oracle.pivoted_lanes(s, eps)
+    wrow = dict(enumerate(oracle.ladder_weight_matrix([mags])[0]))
+    _bound_check(g["xhat"][0], xs, e_pred, g["X"], Xp, wrow)
+
+
+@pytest.mark.slow
+def test_recovered_vs_pivoted_cfg2_geometric_ladder():
+    """The same bar on BASELINE configs[2]'s ladder: 128 geometric magnitudes 1e-1..1e-8
+    (K = 256), two right-hand sides."""
+    w = config(2)
+    s = w.system()
+    B = s.b[:, :2].copy()
+    eps = w.eps()
+    mags = w.ladders[0]
+    g = gpu_run(s, eps, B=B, ladders=w.ladders)
+    assert (g["status"] == 0).all()
+    xs, st = oracle.reference_solve(s, B)
+    e_pred = oracle.predicted_error(s, mags, B)
+    Xp = oracle.pivoted_lanes(s, eps, B)
+    wrow = dict(enumerate(oracle.ladder_weight_matrix(w.ladders)[0]))
+    _bound_check(g["xhat"][0], xs, e_pred, g["X"], Xp, wrow)
