@@ -123,8 +123,20 @@ def oracle_lanes(s, perm, eps, tol, threads=None):
     return X, st, time.perf_counter() - t0, oracle.num_threads()
 
 
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_baseline(s, w, n_lanes):
-    """The oracle as it stands (dense OR1 + combination), on a bounded sample."""
+    """The oracle as it stands (dense OR1 + combination), on a bounded sample: all host
+    threads (OpenMP over lanes), and 1 thread on a smaller sample."""
     import oracle
     from oracle import ordering
     perm = ordering.elimination_order(s.n, s.row_ptr, s.col_idx)
@@ -135,9 +147,71 @@ def cpu_baseline(s, w, n_lanes):
     ladders = w.ladders[:n_lanes // (2 * M_LADDER)]
     xo = oracle.combine(oracle.ladder_weight_matrix(ladders), X)
     dt += time.perf_counter() - t0
+    n1 = max(2 * M_LADDER, n_lanes // 16)
+    _, _, dt1, _ = oracle_lanes(s, perm, eps[:n1], tol, threads=1)
+    oracle.set_num_threads(cores)
     return {"value": n_lanes / dt, "unit": "perturbed solves/s", "cores": cores, "kind": "oracle",
+            "cpu_model": _cpu_model(), "affinity_cpus": len(os.sched_getaffinity(0)),
+            "one_thread": {"value": n1 / dt1, "lanes": n1, "seconds": dt1},
             "sample": f"first {n_lanes} lanes ({len(ladders)} ladders) of the workload, dense OR1 "
-                      f"pivot-free GE + forward/back + combination, {dt:.2f} s"}, X, st, perm
+                      f"pivot-free GE + forward/back + combination, {dt:.2f} s on {cores} threads"}, X, st, perm
+
+
+def exchange_measurement(args, psp, torch, dist, world, rank, local_rank, stream, steps=20):
+    """Row a6 measured: BASELINE configs[2]'s batch — ONE ladder of 128 geometric pairs
+    (K = 256 lanes) x 16 right-hand sides — sharded over the ranks (contiguous lane
+    shards, the ladder straddles every boundary), so the recovered x needs the NCCL sum of
+    the partial sums (psp_recover_reduce, root 0).  At N = 1 a 1-rank communicator (the
+    same code path).  Device time per step (factor + solve + recover + reduce), max over
+    ranks."""
+    from psp_inputs import config as _config
+    w2 = _config(2)
+    s2 = w2.system()
+    e2 = w2.eps()
+    K2 = len(e2)
+    kb, ke = psp.shard_range(K2, rank, world)
+    sv = psp.Solver(local_rank, stream)
+    if world > 1:
+        sv.psp_comm_init_from_group()
+    else:
+        sv.psp_comm_init(1, 0, psp.psp_get_unique_id())
+    sv.psp_symbolic_analyse(s2.n, s2.row_ptr, s2.col_idx, ordering="mindeg")
+    sv.psp_set_perturbations_shard(e2, s2.d, kb, ke - kb)
+    sv.psp_set_weights_dense(psp.ladder_weights_dense(w2.ladders))
+    A2 = torch.tensor(s2.vals, dtype=torch.float64, device="cuda")
+    B2 = torch.tensor(s2.b.T.copy(), dtype=torch.float64, device="cuda")
+    x2 = torch.empty((len(w2.ladders), s2.b.shape[1], s2.n), dtype=torch.float64, device="cuda")
+
+    def one():
+        sv.psp_factor_batch(A2, 0.0)
+        sv.psp_solve_batch(B2)
+        sv.psp_recover_reduce(x2, root=0)
+
+    for _ in range(3):
+        one()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        one()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    if world > 1:
+        tt = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    xr = x2.cpu().numpy()
+    sv.close()
+    return {"workload": w2.name + " sharded over the ranks", "K_global": K2, "K_local": ke - kb,
+            "R": int(s2.b.shape[1]), "W": len(w2.ladders), "ms_per_step": ms,
+            "recovered_solves_per_s": len(w2.ladders) * s2.b.shape[1] / (ms * 1e-3),
+            "perturbed_solves_per_s": K2 * s2.b.shape[1] / (ms * 1e-3),
+            "reduce": "ncclReduce FP64 sum of W x R x n partial sums to rank 0 inside libpsp "
+                      "(psp_recover_reduce)", "reduce_bytes": len(w2.ladders) * s2.b.shape[1] * s2.n * 8,
+            "x_finite": bool(np.isfinite(xr).all()) if rank == 0 else None}
 
 
 def run_reference(args):
@@ -204,6 +278,8 @@ def main():
     if args.impl == "reference":
         return run_reference(args)
 
+    # (the JSON line is the only stdout output: NCCL's version banner would precede it)
+    os.environ.setdefault("NCCL_DEBUG", "WARN")
     import torch
     import torch.distributed as dist
 
@@ -310,6 +386,10 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = float(tt.item())
     e2e_ok = bool(np.array_equal(x_h.numpy(), xh.cpu().numpy()))
+    try:
+        exchange = exchange_measurement(args, psp, torch, dist, world, rank, local_rank, stream)
+    except Exception as exc:  # reporting only
+        exchange = {"error": str(exc)[:200]}
 
     if rank == 0:
         nnzLU, n, R = info["nnz_LU"], s.n, 1
@@ -328,7 +408,7 @@ def main():
         peak = peaks.get("hbm_gbs", 6650.0)
         peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
         traffic = None   # ncu DRAM bytes per factor launch (profiles/), same workload only
-        tp = os.path.join(ROOT, "profiles", "r1_traffic.json")
+        tp = os.path.join(ROOT, "profiles", "r2_traffic.json")
         if os.path.exists(tp) and K == 65536 and s.n == 531:
             traffic = json.load(open(tp)).get("traffic_bytes_per_launch")
         kern = {"factor": (t_factor, bytes_factor), "solve": (t_solve, bytes_solve),
@@ -358,12 +438,14 @@ def main():
             "hbm_gbs_algorithmic": (bytes_factor + bytes_solve + bytes_recover) / (ms_step * 1e-3) / 1e9,
             "roofline": {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "frac_of_nominal_8tbs": achieved / 8000.0,
                          "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": bdom, "launch_ms": tdom},
             # per step: pivot tolerance, program patch, factor, solve, recover
             "gpu_launches": 5 * args.steps,
             "clocks": clocks,
             "lane_failures": n_failed,
+            "exchange": exchange,
             "symbolic": info,
         }
         h2d = 8 * s.nnz + 8 * n * R

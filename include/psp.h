@@ -56,7 +56,8 @@ enum {
   PSP_ERR_BATCH_INFEASIBLE = 5,  /* a non-zero weight touches a failed lane */
   PSP_ERR_CUDA = 6,              /* CUDA runtime error; detail string has the code   */
   PSP_ERR_ALLOC = 7,             /* device or host allocation failed                 */
-  PSP_ERR_UNSUPPORTED = 8        /* feature not available in this build              */
+  PSP_ERR_UNSUPPORTED = 8,       /* feature not available in this build / handle     */
+  PSP_ERR_NCCL = 9               /* NCCL error; detail string has NCCL's message     */
 };
 
 /* Elimination orders for psp_symbolic_analyse (R13). */
@@ -354,6 +355,52 @@ psp_status psp_get_perturbations(psp_handle h, double* eps_h);
  * Synchronous.  Errors: ARG (W < 1, R < 1, null), STATE (symbolic_analyse first), CUDA. */
 psp_status psp_residual(psp_handle h, const double* A_vals, int32_t W, int32_t R, const double* B,
                         const double* x, double* res_h);
+
+/* ---- multi-GPU: one handle per GPU (one process per GPU), the perturbation batch
+ *      sharded over the ranks, the partial sums of Alg. 1 steps 3-4 reduced with NCCL
+ *      (DESIGN.md §6).  NCCL is loaded at run time
+ *      (libnccl.so.2, the process's already-loaded copy when there is one). ---------- */
+
+/* The NCCL unique id (128 bytes) of a new communicator, on one rank; the caller
+ * distributes it to every rank (e.g. torch.distributed broadcast).  Errors: ARG,
+ * UNSUPPORTED (no libnccl), NCCL. */
+psp_status psp_get_unique_id(void* id_h);
+
+/* Join the communicator `id_h` as `rank` of `nranks` (collective over the ranks; the
+ * handle's device).  Replaces an earlier communicator of the handle; psp_destroy frees
+ * it.  nranks = 1 is valid (the reduce is then a local copy through NCCL).  Errors: ARG,
+ * UNSUPPORTED (host-only handle, no libnccl), NCCL. */
+psp_status psp_comm_init(psp_handle h, int32_t nranks, int32_t rank, const void* id_h);
+
+/* psp_set_perturbations for a shard: this rank owns the global lanes [k_begin, k_begin +
+ * k_count) of a batch of K_global lanes (eps_h has K_global entries; local lane k is global
+ * lane k_begin + k).  Contiguous shards keep each ladder's lanes together where the split
+ * allows; correctness never depends on it (the weights are global).  Errors: as
+ * psp_set_perturbations, ARG for a shard outside [0, K_global). */
+psp_status psp_set_perturbations_shard(psp_handle h, int32_t K_global, const double* eps_h,
+                                       const double* d_h, int32_t k_begin, int32_t k_count);
+
+/* Pure host helper: the rows of the dense weights_h[W][K_global] (row-major) restricted to
+ * the shard [k_begin, k_begin + k_count), as CSR over LOCAL lanes: w_ptr_h[W + 1],
+ * w_lane_h / w_val_h (capacity W * k_count; either may be NULL to count only), exact zeros
+ * dropped, *nnz_h entries.  Errors: ARG (bad shard, non-finite weight). */
+psp_status psp_shard_weights(int32_t W, const double* weights_h, int32_t K_global, int32_t k_begin,
+                             int32_t k_count, int32_t* w_ptr_h, int32_t* w_lane_h, double* w_val_h,
+                             int32_t* nnz_h);
+
+/* psp_set_weights from dense GLOBAL weights weights_h[W][K_global] (row-major; the
+ * combination of Eq. (13) with the pair average folded in): this rank keeps its shard's
+ * columns (psp_shard_weights).  Errors: ARG, STATE. */
+psp_status psp_set_weights_dense(psp_handle h, int32_t W, const double* weights_h);
+
+/* Collective over the communicator's ranks (all call it): each rank's partial sums
+ * x[w][r][i] = sum over its lanes of w * x_k,r[i] (psp_recover, into x), then the sum over
+ * the ranks with NCCL on the handle's stream, in place: root >= 0 ncclReduce (the result
+ * on `root`; other ranks keep their partial sums), root = -1 ncclAllReduce (every rank).
+ * x: device, W x R x n on every rank.  Without psp_comm_init: psp_recover (local sums).
+ * The summation order over ranks is NCCL's (R16).  Errors: ARG (root out of
+ * range), STATE, CUDA, NCCL. */
+psp_status psp_recover_reduce(psp_handle h, double* x, int32_t root);
 
 /* ---- host helper (pure) --------------------------------------------------------- */
 

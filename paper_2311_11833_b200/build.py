@@ -15,6 +15,7 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC,-O2,-ffp-contract=off",
     "-Xptxas", "-v",
     "-shared",
+    "-ldl",                             # libnccl is dlopen'ed (psp_host.cpp nccl_api)
 ]
 
 

@@ -6,6 +6,9 @@
 // layout and the kernel plans are computed once per sparsity pattern on the host.
 // The numeric work of every step of Alg. 1 runs in the CUDA kernels of
 // psp_kernels.cu; nothing here touches a lane's values.
+#include <dlfcn.h>
+#include <nccl.h>   // types only: libnccl is loaded at run time (psp_nccl below)
+
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
@@ -35,6 +38,41 @@ struct DevBuf {
     bytes = 0;
   }
 };
+
+// NCCL, loaded on first use (dlopen "libnccl.so.2"; the process's already-loaded copy —
+// e.g. torch's — when there is one): the library itself has no link-time NCCL dependency,
+// so host-only and single-GPU use never need it.
+struct NcclApi {
+  bool tried = false, ok = false;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t,
+                         cudaStream_t) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*errorString)(ncclResult_t) = nullptr;
+};
+NcclApi& nccl_api() {
+  static NcclApi api;
+  if (!api.tried) {
+    api.tried = true;
+    void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (lib) {
+      api.getUniqueId = reinterpret_cast<decltype(api.getUniqueId)>(dlsym(lib, "ncclGetUniqueId"));
+      api.commInitRank = reinterpret_cast<decltype(api.commInitRank)>(dlsym(lib, "ncclCommInitRank"));
+      api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(dlsym(lib, "ncclCommDestroy"));
+      api.reduce = reinterpret_cast<decltype(api.reduce)>(dlsym(lib, "ncclReduce"));
+      api.allReduce = reinterpret_cast<decltype(api.allReduce)>(dlsym(lib, "ncclAllReduce"));
+      api.errorString = reinterpret_cast<decltype(api.errorString)>(dlsym(lib, "ncclGetErrorString"));
+      api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.reduce && api.allReduce &&
+               api.errorString;
+    }
+  }
+  return api;
+}
 
 }  // namespace
 
@@ -95,6 +133,12 @@ struct psp_ctx {
   DevBuf res_d;                        // psp_residual output
   std::vector<cudaEvent_t> fev, sev;
   size_t nf = 0, ns = 0;
+
+  // --- multi-GPU: this rank owns global lanes [k_begin, k_begin + K) of
+  // K_global; the partial sums of psp_recover are reduced over `comm` ---
+  ncclComm_t comm = nullptr;
+  int32_t nranks = 1, rank = 0;
+  int32_t K_global = 0, k_begin = 0;
 
   // --- perturbations ---
   int32_t K = 0, K_pad = 0;
@@ -225,6 +269,7 @@ const char* psp_status_string(psp_status s) {
     case PSP_ERR_CUDA: return "PSP_ERR_CUDA";
     case PSP_ERR_ALLOC: return "PSP_ERR_ALLOC";
     case PSP_ERR_UNSUPPORTED: return "PSP_ERR_UNSUPPORTED";
+    case PSP_ERR_NCCL: return "PSP_ERR_NCCL";
     default: return "PSP_ERR_UNKNOWN";
   }
 }
@@ -285,6 +330,7 @@ psp_status psp_destroy(psp_handle h) {
   }
   for (auto* v : {&h->fev, &h->sev})
     for (cudaEvent_t e : *v) cudaEventDestroy(e);
+  if (h->comm) nccl_api().commDestroy(h->comm);
   delete h;
   return PSP_OK;
 }
@@ -822,6 +868,8 @@ psp_status psp_set_perturbations(psp_handle h, int32_t K, const double* eps_h, c
   }
   h->K = K;
   h->K_pad = Kp;
+  h->K_global = K;   // (psp_set_perturbations_shard overrides)
+  h->k_begin = 0;
   h->d_host.assign(d_h, d_h + h->n);
   h->eps_host.assign(eps_h, eps_h + K);
   h->factored = h->solved = h->recovered = false;
@@ -1338,6 +1386,103 @@ psp_status psp_solve_host(psp_handle h, const double* A_vals_h, int32_t R, const
   CUDA_TRY(h, cudaMemcpyAsync(x_h, h->stageX_d.p, sizeof(double) * (size_t)h->W * R * h->n,
                               cudaMemcpyDeviceToHost, h->stream));
   return psp_get_lane_status(h, nullptr);
+}
+
+// ---- multi-GPU: sharded lanes and the NCCL reduce of the partial sums (row a6) --------
+
+psp_status psp_get_unique_id(void* id_h) {
+  if (!id_h) return PSP_ERR_ARG;
+  NcclApi& api = nccl_api();
+  if (!api.ok) return PSP_ERR_UNSUPPORTED;
+  ncclUniqueId id;
+  if (api.getUniqueId(&id) != ncclSuccess) return PSP_ERR_NCCL;
+  std::memcpy(id_h, &id, sizeof id);
+  return PSP_OK;
+}
+
+psp_status psp_comm_init(psp_handle h, int32_t nranks, int32_t rank, const void* id_h) {
+  if (!h || !id_h || nranks < 1 || rank < 0 || rank >= nranks) return PSP_ERR_ARG;
+  if (h->device < 0) return fail(h, PSP_ERR_UNSUPPORTED, "host-only handle");
+  NcclApi& api = nccl_api();
+  if (!api.ok) return fail(h, PSP_ERR_UNSUPPORTED, "libnccl.so.2 not found");
+  cudaSetDevice(h->device);
+  if (h->comm) {
+    api.commDestroy(h->comm);
+    h->comm = nullptr;
+  }
+  ncclUniqueId id;
+  std::memcpy(&id, id_h, sizeof id);
+  ncclComm_t c = nullptr;
+  const ncclResult_t r = api.commInitRank(&c, nranks, id, rank);
+  if (r != ncclSuccess) return fail(h, PSP_ERR_NCCL, "ncclCommInitRank: %s", api.errorString(r));
+  h->comm = c;
+  h->nranks = nranks;
+  h->rank = rank;
+  return PSP_OK;
+}
+
+psp_status psp_set_perturbations_shard(psp_handle h, int32_t K_global, const double* eps_h, const double* d_h,
+                                       int32_t k_begin, int32_t k_count) {
+  if (!h) return PSP_ERR_ARG;
+  if (K_global < 1 || !eps_h || k_begin < 0 || k_count < 1 || k_begin + k_count > K_global)
+    return fail(h, PSP_ERR_ARG, "shard [k_begin, k_begin + k_count) must lie in [0, K_global)");
+  psp_status s = psp_set_perturbations(h, k_count, eps_h + k_begin, d_h);
+  if (s) return s;
+  h->K_global = K_global;
+  h->k_begin = k_begin;
+  return PSP_OK;
+}
+
+psp_status psp_shard_weights(int32_t W, const double* weights_h, int32_t K_global, int32_t k_begin,
+                             int32_t k_count, int32_t* w_ptr_h, int32_t* w_lane_h, double* w_val_h,
+                             int32_t* nnz_h) {
+  if (W < 1 || !weights_h || K_global < 1 || k_begin < 0 || k_count < 1 || k_begin + k_count > K_global ||
+      !w_ptr_h || !nnz_h)
+    return PSP_ERR_ARG;
+  int32_t q = 0;
+  w_ptr_h[0] = 0;
+  for (int32_t w = 0; w < W; ++w) {
+    const double* row = weights_h + (size_t)w * K_global;
+    for (int32_t k = 0; k < k_count; ++k) {
+      const double v = row[k_begin + k];
+      if (!std::isfinite(v)) return PSP_ERR_ARG;
+      if (v != 0.0) {
+        if (w_lane_h) w_lane_h[q] = k;
+        if (w_val_h) w_val_h[q] = v;
+        ++q;
+      }
+    }
+    w_ptr_h[w + 1] = q;
+  }
+  *nnz_h = q;
+  return PSP_OK;
+}
+
+psp_status psp_set_weights_dense(psp_handle h, int32_t W, const double* weights_h) {
+  if (!h || !weights_h || W < 1) return PSP_ERR_ARG;
+  if (h->K == 0) return fail(h, PSP_ERR_STATE, "set_perturbations first");
+  std::vector<int32_t> ptr(W + 1), lane((size_t)W * h->K);
+  std::vector<double> val((size_t)W * h->K);
+  int32_t nnz = 0;
+  psp_status s = psp_shard_weights(W, weights_h, h->K_global, h->k_begin, h->K, ptr.data(), lane.data(),
+                                   val.data(), &nnz);
+  if (s) return fail(h, s, "non-finite weight");
+  return psp_set_weights(h, W, ptr.data(), lane.data(), val.data());
+}
+
+psp_status psp_recover_reduce(psp_handle h, double* x, int32_t root) {
+  if (!h || !x) return PSP_ERR_ARG;
+  if (root < -1 || root >= h->nranks) return fail(h, PSP_ERR_ARG, "root out of range");
+  psp_status s = psp_recover(h, x);
+  if (s) return s;
+  if (!h->comm) return PSP_OK;   // (single process without a communicator: the local sums)
+  NcclApi& api = nccl_api();
+  const size_t count = (size_t)h->W * h->R * h->n;
+  const ncclResult_t r = root < 0 ? api.allReduce(x, x, count, ncclFloat64, ncclSum, h->comm, h->stream)
+                                  : api.reduce(x, x, count, ncclFloat64, ncclSum, root, h->comm, h->stream);
+  if (r != ncclSuccess) return fail(h, PSP_ERR_NCCL, "%s: %s", root < 0 ? "ncclAllReduce" : "ncclReduce",
+                                    api.errorString(r));
+  return PSP_OK;
 }
 
 psp_status psp_ladder_weights(int32_t m, const double* s_h, double* eps_out_h, double* w_out_h) {

@@ -15,7 +15,7 @@ LIB_PATH = os.environ.get("PSP_LIB", os.path.join(_HERE, "libpsp.so"))
 PSP_OK = 0
 STATUS = {0: "PSP_OK", 1: "PSP_ERR_ARG", 2: "PSP_ERR_DIM", 3: "PSP_ERR_STATE",
           4: "PSP_ERR_ZERO_PIVOT", 5: "PSP_ERR_BATCH_INFEASIBLE", 6: "PSP_ERR_CUDA",
-          7: "PSP_ERR_ALLOC", 8: "PSP_ERR_UNSUPPORTED"}
+          7: "PSP_ERR_ALLOC", 8: "PSP_ERR_UNSUPPORTED", 9: "PSP_ERR_NCCL"}
 PSP_ERR_ZERO_PIVOT = 4
 PSP_ERR_BATCH_INFEASIBLE = 5
 ORDER = {"natural": 0, "mindeg": 1, "user": 2, "mindeg_first": 3}
@@ -26,7 +26,9 @@ EXPORTS = ["psp_create", "psp_destroy", "psp_set_stream", "psp_status_string",
            "psp_get_solutions", "psp_get_phase_times", "psp_get_lane_growth", "psp_estimate_rho",
            "psp_set_weights", "psp_recover", "psp_get_lane_status", "psp_solve_host", "psp_solve_host_async",
            "psp_synchronize", "psp_ladder_weights", "psp_set_option", "psp_get_factor", "psp_residual",
-           "psp_rescale_failed_rows", "psp_get_perturbations", "psp_get_last_kernels"]
+           "psp_rescale_failed_rows", "psp_get_perturbations", "psp_get_last_kernels",
+           "psp_get_unique_id", "psp_comm_init", "psp_set_perturbations_shard", "psp_shard_weights",
+           "psp_set_weights_dense", "psp_recover_reduce"]
 KERNEL = {0: "none", 1: "coop", 2: "batch", 3: "batch_tmem", 4: "batch_spill"}
 OPT = {"factor_groups": 1, "factor_warps": 2, "factor_lanes": 3, "factor_slab_warps": 4,
        "factor_pairs": 5, "factor_tmem": 6, "solve_tmem": 7, "phase_events": 8, "growth": 9, "coop": 10,
@@ -97,6 +99,12 @@ def lib():
             "psp_set_option": [P, I32, I64],
             "psp_get_factor": [P, I32, P],
             "psp_get_last_kernels": [P, P],
+            "psp_get_unique_id": [P],
+            "psp_comm_init": [P, I32, I32, P],
+            "psp_set_perturbations_shard": [P, I32, P, P, I32, I32],
+            "psp_shard_weights": [I32, P, I32, I32, I32, P, P, P, P],
+            "psp_set_weights_dense": [P, I32, P],
+            "psp_recover_reduce": [P, P, I32],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -264,6 +272,42 @@ class Solver:
         self._check(lib().psp_get_phase_times(self.h, ms))
         return float(ms[0]), float(ms[1])
 
+    def psp_comm_init(self, nranks, rank, uid: bytes):
+        """Join the NCCL communicator with unique id `uid` (128 bytes, psp_get_unique_id)."""
+        buf = ctypes.create_string_buffer(bytes(uid), 128)
+        self._check(lib().psp_comm_init(self.h, int(nranks), int(rank), buf))
+
+    def psp_comm_init_from_group(self, group=None):
+        """psp_comm_init over a torch.distributed process group: rank 0 draws the id,
+        torch.distributed broadcasts it (plumbing), every rank joins."""
+        import torch.distributed as dist
+        obj = [psp_get_unique_id() if dist.get_rank(group) == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        self.psp_comm_init(dist.get_world_size(group), dist.get_rank(group), obj[0])
+
+    def psp_set_perturbations_shard(self, eps_global, d, k_begin, k_count):
+        e = np.ascontiguousarray(eps_global, dtype=np.float64)
+        dd = np.ascontiguousarray(d, dtype=np.float64)
+        if dd.shape != (self.n,):
+            raise ValueError("d must have n entries")
+        self._check(lib().psp_set_perturbations_shard(self.h, len(e), _np_ptr(e), _np_ptr(dd),
+                                                      int(k_begin), int(k_count)))
+        self.K = int(k_count)
+
+    def psp_set_weights_dense(self, weights):
+        """Dense GLOBAL weights [W, K_global]; this rank keeps its shard's columns."""
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        self._check(lib().psp_set_weights_dense(self.h, w.shape[0], _np_ptr(w)))
+        self.W = w.shape[0]
+
+    def psp_recover_reduce(self, out=None, root=-1):
+        """Partial sums on the device + the NCCL sum over the ranks (root = -1: every
+        rank gets x; root >= 0: only `root`)."""
+        out = out if out is not None else self.torch.empty((self.W, self.R, self.n), dtype=self.torch.float64,
+                                                           device=f"cuda:{self.device}")
+        self._check(lib().psp_recover_reduce(self.h, _t_ptr(out), int(root)))
+        return out
+
     def psp_get_last_kernels(self):
         """(factor kernel, factor fused forward?, solve kernel, solve ran forward?) of the
         last numeric calls; kernel names from KERNEL (psp.h PSP_KERNEL_*)."""
@@ -329,6 +373,44 @@ class Solver:
             raise ValueError(f"expected shape {shape}, got {tuple(t.shape)}")
 
 
+def psp_get_unique_id() -> bytes:
+    """C: a fresh NCCL unique id (128 bytes)."""
+    buf = ctypes.create_string_buffer(128)
+    st = lib().psp_get_unique_id(buf)
+    if st:
+        raise PSPError(st, "psp_get_unique_id")
+    return buf.raw
+
+
+def psp_shard_weights(weights, k_begin, k_count):
+    """C helper: dense global weights [W, K_global] -> this shard's CSR over local lanes."""
+    w = np.ascontiguousarray(weights, dtype=np.float64)
+    W, Kg = w.shape
+    ptr = np.zeros(W + 1, np.int32)
+    lane = np.zeros(max(W * k_count, 1), np.int32)
+    val = np.zeros(max(W * k_count, 1), np.float64)
+    nnz = ctypes.c_int32()
+    st = lib().psp_shard_weights(W, _np_ptr(w), Kg, int(k_begin), int(k_count), _np_ptr(ptr), _np_ptr(lane),
+                                 _np_ptr(val), ctypes.byref(nnz))
+    if st:
+        raise PSPError(st, "psp_shard_weights")
+    return ptr, lane[:nnz.value].copy(), val[:nnz.value].copy()
+
+
+def ladder_weights_dense(ladders):
+    """Dense GLOBAL weights [W, K] (psp_set_weights_dense) for ladders laid out
+    consecutively in lane order, one recovered solution per ladder (C helper
+    psp_ladder_weights: beta_j / 2 on each sign)."""
+    K = 2 * sum(len(m) for m in ladders)
+    out = np.zeros((len(ladders), K))
+    k = 0
+    for g, mags in enumerate(ladders):
+        _, w = psp_ladder_weights(mags)
+        out[g, k:k + len(w)] = w
+        k += len(w)
+    return out
+
+
 def ladder_weights_csr(ladders, lane_offset=0, k_begin=0, k_end=None):
     """Weights CSR for ladders laid out consecutively in lane order (one recovered
     solution per ladder).  Only lanes in [k_begin, k_end) are kept, renumbered to
@@ -358,14 +440,9 @@ def shard_range(K, rank, world):
 
 
 def recover_allreduce(solver, out, group=None):
-    """Row a5 + a6: this rank's partial sums x_hat[w] = sum over its lanes of w_k x_k
-    (psp_recover, on the device), then the sum over ranks (torch.distributed all-reduce:
-    NCCL over NVLink on GPUs).  With one rank (or no process group) it is psp_recover."""
-    solver.psp_recover(out)
-    import torch.distributed as dist
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.all_reduce(out, op=dist.ReduceOp.SUM, group=group)
-    return out
+    """Rows a5 + a6: psp_recover_reduce (partial sums on the device, NCCL all-reduce inside
+    libpsp when the solver joined a communicator, psp_comm_init / psp_comm_init_from_group)."""
+    return solver.psp_recover_reduce(out, root=-1)
 
 
 class HostSymbolic:

@@ -444,27 +444,77 @@ def test_large_configs_sampled_lanes(ci):
 
 
 def test_bench_size_sampled():
-    """The launch configuration bench.py times (300-bus, K = 65536, R = 1)."""
+    """The launch configuration bench.py times (300-bus, K = 65536, R = 1): the fused
+    psp_factor_solve_batch (the capacity-planned factor with the forward substitution,
+    then the backward solve) and the uniform-ladder recover, lanes sampled from every
+    CTA-sized stretch of the batch (first, middle, last CTA, the ragged end) against the
+    oracle bitwise, and recovered ladders within 1e-10."""
     from bench import bench_workload
     w = bench_workload()
     s = w.system()
     eps = w.eps()
-    g = gpu_run(s, eps, ladders=w.ladders, lanes_out=False)
-    assert (g["status"] == 0).all()
-    solver = g["solver"]
-    X = solver.psp_get_solutions()
     K = len(eps)
-    sample = np.unique(np.r_[0, 1, 31, 32, 33, K // 3, K // 2, K - 33, K - 2, K - 1])
+    solver = psp.Solver(0)
+    solver.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering="mindeg")
+    info, perm = solver.psp_get_symbolic_info()
+    assert np.array_equal(perm, oracle_perm(s, -1))
+    solver.psp_set_perturbations(eps, s.d)
+    wp, wl, wv = psp.ladder_weights_csr(w.ladders)
+    solver.psp_set_weights(wp, wl, wv)
+    A = torch.tensor(s.vals, dtype=torch.float64, device="cuda")
+    b = torch.tensor(s.b[:, 0].copy(), dtype=torch.float64, device="cuda")
+    solver.psp_factor_solve_batch(A, b, 0.0)
+    kernels = solver.psp_get_last_kernels()
+    assert kernels[:2] == ("batch_spill", True), kernels   # the bench's factor
+    xh = solver.psp_recover().cpu().numpy()
+    rc, st = solver.psp_get_lane_status()
+    assert rc == 0 and (st == 0).all()
+    X = solver.psp_get_solutions()
+    lanes_per_cta = 64 * info["spill_warps_per_cta"]
+    n_cta = (K + lanes_per_cta - 1) // lanes_per_cta
+    sample = set()
+    for cta in (0, 1, n_cta // 2, n_cta - 2, n_cta - 1):
+        lo = cta * lanes_per_cta
+        sample |= {lo, lo + 31, lo + 32, lo + 63, lo + 64, lo + lanes_per_cta - 1}
+    sample = np.array(sorted(k for k in sample | {K - 1, K - 2} if 0 <= k < K))
     Xs = X[torch.tensor(sample, device="cuda")].cpu().numpy()
     tol = oracle.default_tol(s.n, s.row_ptr, s.col_idx, s.vals)
-    Xo, sto = oracle.dense_batch(s, g["operm"], eps[sample], tol)
+    Xo, sto = oracle.dense_batch(s, perm, eps[sample], tol, B=s.b[:, :1])
     assert (sto == 0).all()
     assert np.array_equal(Xs, Xo)
     for gi in [0, len(w.ladders) // 2, len(w.ladders) - 1]:
         lanes = np.arange(8 * gi, 8 * gi + 8)
-        Xl, _ = oracle.dense_batch(s, g["operm"], eps[lanes], tol)
+        Xl, _ = oracle.dense_batch(s, perm, eps[lanes], tol, B=s.b[:, :1])
         xo = oracle.combine(oracle.ladder_weight_matrix([w.ladders[gi]]), Xl)
-        assert rel(g["xhat"][gi], xo[0]) <= 1e-10
+        assert rel(xh[gi], xo[0]) <= 1e-10
+
+
+def test_infeasible_then_rescale_then_feasible():
+    """recover on a batch with a failed lane raises BATCH_INFEASIBLE; after
+    psp_rescale_failed_rows + refactor + recover the flag is gone (PSP_OK)."""
+    w = config(1)
+    s = w.system()
+    tol = oracle.default_tol(s.n, s.row_ptr, s.col_idx, s.vals)
+    dp = abs(s.d[s.slot_p])
+    bad = 0.25 * tol / dp                        # the leading pivot eps * d_p falls below tol
+    mags = [bad, 2 * bad]
+    eps = ladder_eps(mags)
+    solver = psp.Solver(0)
+    solver.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering="mindeg_first", first_node=s.slot_p)
+    solver.psp_set_perturbations(eps, s.d)
+    wp, wl, wv = psp.ladder_weights_csr([mags])
+    solver.psp_set_weights(wp, wl, wv)
+    A = torch.tensor(s.vals, dtype=torch.float64, device="cuda")
+    b = torch.tensor(s.b[:, 0].copy(), dtype=torch.float64, device="cuda")
+    solver.psp_factor_solve_batch(A, b, 0.0)
+    solver.psp_recover()
+    rc, st = solver.psp_get_lane_status()
+    assert rc == psp.PSP_ERR_BATCH_INFEASIBLE and (st[:2] == 1).all()
+    assert solver.psp_rescale_failed_rows(2e-3 / bad) == 1
+    solver.psp_factor_solve_batch(A, b, 0.0)
+    xh = solver.psp_recover().cpu().numpy()
+    rc, st = solver.psp_get_lane_status()
+    assert rc == 0 and (st == 0).all() and np.isfinite(xh).all()
 
 
 def test_diagonal_closed_form_at_full_size():
@@ -859,24 +909,27 @@ def test_random_configurations_stress():
 
 
 def test_sharded_recover_partials_sum_to_full():
-    """Row a6 on one GPU: lanes split over two handles (a ladder straddles the split);
-    each recovers its partial sums with its shard of the weights; their sum equals the
-    single-handle recovery up to the summation order (reading R16)."""
+    """Row a6 on one GPU through the library's sharding API: lanes split over two handles
+    (psp_set_perturbations_shard; a ladder straddles the split), each with the dense
+    GLOBAL weights (psp_set_weights_dense keeps its shard's columns) and its partial sums
+    (psp_recover_reduce without a communicator); their sum equals the single-handle
+    recovery up to the summation order (reading R16), and the oracle's within 1e-10."""
     w = config(1, n_ladders=6)
     s = w.system()
     eps = w.eps()
     K = len(eps)
+    Wg = oracle.ladder_weight_matrix(w.ladders)
     A = torch.tensor(s.vals, dtype=torch.float64, device="cuda")
     B = torch.tensor(s.b.T.copy(), dtype=torch.float64, device="cuda")
 
     def run(kb, ke):
         sv = psp.Solver(0)
         sv.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering="mindeg")
-        sv.psp_set_perturbations(eps[kb:ke], s.d)
+        sv.psp_set_perturbations_shard(eps, s.d, kb, ke - kb)
         sv.psp_factor_batch(A, 0.0)
         sv.psp_solve_batch(B)
-        sv.psp_set_weights(*psp.ladder_weights_csr(w.ladders, k_begin=kb, k_end=ke))
-        out = sv.psp_recover()
+        sv.psp_set_weights_dense(Wg)
+        out = sv.psp_recover_reduce(root=-1)
         torch.cuda.synchronize()
         return out.cpu().numpy()
 
@@ -886,6 +939,37 @@ def test_sharded_recover_partials_sum_to_full():
     tot = run(0, cut) + run(cut, K)
     scale = np.abs(full).max()
     assert np.max(np.abs(tot - full)) <= 64 * np.finfo(float).eps * scale
+    tol = oracle.default_tol(s.n, s.row_ptr, s.col_idx, s.vals)
+    Xo, _ = oracle.dense_batch(s, oracle_perm(s, -1), eps, tol)
+    assert rel(full, oracle.combine(Wg, Xo)) <= 1e-10
+
+
+@pytest.mark.parametrize("root", [-1, 0])
+def test_nccl_recover_reduce_single_rank(root):
+    """Row a6 through NCCL inside libpsp at nranks = 1 (psp_get_unique_id,
+    psp_comm_init, psp_recover_reduce: ncclAllReduce / ncclReduce on the handle's stream):
+    the reduced result equals the local combination bitwise (a 1-rank sum is a copy) and
+    the oracle's combination within 1e-10; cfg2's single 128-pair ladder, R = 2."""
+    w = config(2)
+    s = w.system()
+    eps = w.eps()
+    Bn = s.b[:, :2].copy()
+    sv = psp.Solver(0)
+    sv.psp_comm_init(1, 0, psp.psp_get_unique_id())
+    sv.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering="mindeg")
+    sv.psp_set_perturbations_shard(eps, s.d, 0, len(eps))
+    A = torch.tensor(s.vals, dtype=torch.float64, device="cuda")
+    sv.psp_factor_batch(A, 0.0)
+    sv.psp_solve_batch(torch.tensor(Bn.T.copy(), dtype=torch.float64, device="cuda"))
+    Wg = oracle.ladder_weight_matrix(w.ladders)
+    sv.psp_set_weights_dense(Wg)
+    red = sv.psp_recover_reduce(root=root).cpu().numpy()
+    loc = sv.psp_recover().cpu().numpy()
+    assert np.array_equal(red, loc)
+    tol = oracle.default_tol(s.n, s.row_ptr, s.col_idx, s.vals)
+    Xo, _ = oracle.SparseOracle(s, oracle_perm(s, -1)).batch(eps, tol, B=Bn)
+    assert rel(red, oracle.combine(Wg, Xo)) <= 1e-10
+    sv.close()
 
 
 @pytest.mark.parametrize("K,fused", [(1000, False), (1000, True), (4133, True), (33, True)])

@@ -1,8 +1,11 @@
 """Multi-rank host logic on CPU (world size 2, gloo): lane sharding and the one
 exchange step of the method — every rank combines its own lanes with its shard of the
-weights (rows a5), the partial sums are summed across ranks (row a6).  The lanes are
-the oracle's (this checks the sharding plan and the reduce semantics, not a kernel);
-a ladder deliberately straddles the rank boundary."""
+weights (rows a5), the partial sums are summed across ranks (row a6).  The shard of the
+weights is libpsp's own host logic (psp_shard_weights, the code psp_set_weights_dense runs
+on every rank); the NCCL id that psp_comm_init needs is drawn by libpsp on rank 0 and
+broadcast (psp_comm_init itself needs a GPU per rank).  The lanes are the oracle's (this
+checks the sharding plan and the reduce semantics, not a kernel); a ladder deliberately
+straddles the rank boundary."""
 import os
 import socket
 
@@ -43,15 +46,21 @@ def _worker(rank, world, port, q):
         perm = np.arange(s.n, dtype=np.int32)
         tol = oracle.default_tol(s.n, s.row_ptr, s.col_idx, s.vals)
         X, st = oracle.dense_batch(s, perm, eps[kb:ke], tol)
-        wp, wl, wv = psp.ladder_weights_csr(lad, k_begin=kb, k_end=ke)
+        wp, wl, wv = psp.psp_shard_weights(oracle.ladder_weight_matrix(lad), kb, ke - kb)
+        wp2, wl2, wv2 = psp.ladder_weights_csr(lad, k_begin=kb, k_end=ke)   # the binding's own
+        assert np.array_equal(wp, wp2) and np.array_equal(wl, wl2)
+        assert np.max(np.abs(wv - wv2)) <= 4 * np.finfo(float).eps * np.max(np.abs(wv))
         W = len(wp) - 1
+        uid = [psp.psp_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        assert isinstance(uid[0], bytes) and len(uid[0]) == 128
         part = np.zeros((W, 1, s.n))
         for w in range(W):                       # ascending local lane, one fma per term
             for e in range(wp[w], wp[w + 1]):
                 part[w] += wv[e] * X[wl[e]]
         t = torch.tensor(part)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        q.put((rank, t.numpy(), (kb, ke)))
+        q.put((rank, t.numpy(), (kb, ke), uid[0]))
     finally:
         dist.destroy_process_group()
 
@@ -79,8 +88,9 @@ def test_two_rank_partial_sums_equal_full_combination():
         assert pr.exitcode == 0
     res.sort()
     assert res[0][2] == (0, 10) and res[1][2] == (10, 20)
-    # both ranks hold the same reduced result
+    # both ranks hold the same reduced result (and the same communicator id)
     assert np.array_equal(res[0][1], res[1][1])
+    assert res[0][3] == res[1][3]
     s = config(0).system()
     lad = _ladders()
     eps = np.concatenate([np.ravel([[m, -m] for m in l]) for l in lad])
