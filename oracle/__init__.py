@@ -163,6 +163,33 @@ def dense_batch(sysm, perm, eps, tol, B=None):
     return X, st
 
 
+def dense_D_batch(A, Dm, perm, eps, tol, B):
+    """OR1 with a general (dense, non-diagonal) perturbation matrix D (SURVEY §8(f) 3;
+    the footnote at P:L72 and P:L314 "all entries of the perturbation matrix ... normally
+    distributed"): per lane k, A_k = P (A + eps_k D) P^T entry by entry (one product, one
+    sum: a_ij + (eps_k * D_ij)), then the same pivot-free elimination and substitutions as
+    dense_batch (lu_nopivot, lu_solve).  A, Dm: n x n dense (original ordering); B: n x R.
+    Returns X [K, R, n] (original ordering) and status [K] (0, or 1 + first failing
+    pivot position; a failed lane's X is NaN)."""
+    A = np.asarray(A, dtype=np.float64)
+    Dm = np.asarray(Dm, dtype=np.float64)
+    perm = np.asarray(perm, dtype=np.int64)
+    B = np.asarray(B, dtype=np.float64).reshape(A.shape[0], -1)
+    n, R = A.shape[0], B.shape[1]
+    eps = np.asarray(eps, dtype=np.float64)
+    X = np.full((len(eps), R, n), np.nan)
+    st = np.zeros(len(eps), dtype=np.int32)
+    for k, e in enumerate(eps):
+        Ak = A + e * Dm                        # elementwise: a_ij + (e * D_ij), two roundings
+        LU, st[k] = lu_nopivot(Ak[np.ix_(perm, perm)], tol)
+        if st[k]:
+            continue
+        for r in range(R):
+            y = lu_solve(LU, B[perm, r])
+            X[k, r, perm] = y
+    return X, st
+
+
 class SparseOracle:
     """OR2: the oracle's own symbolic (ordering.filled_pattern) + sparse numeric."""
 
@@ -266,7 +293,7 @@ def pivoted_lanes(sysm, eps, B=None):
     return out
 
 
-def predicted_error(sysm, mags, B=None):
+def predicted_error(sysm, mags, B=None, Dm=None):
     """Theorem 1's truncation error with its constant, exactly: the identity (I3) of
     SURVEY §8(c) (Lagrange interpolation of t -> (I - t M^2)^{-1} x* at the nodes
     t_j = s_j^2, evaluated at t = 0; Remark 2's beta are that Lagrange basis, P:L197-203;
@@ -281,21 +308,23 @@ def predicted_error(sysm, mags, B=None):
         of Eq. (avg_hats), since (I + s M)^{-1} = (A + s D)^{-1} A).
     The factors commute (functions of M^2); each step applies t_j M^2 (I - t_j M^2)^{-1}
     so that neither prod t_j nor M^{2m} is formed on its own (no under/overflow for long
-    ladders).  Returns e_pred [R, n] (original ordering)."""
+    ladders).  Dm: a dense n x n perturbation matrix in place of diag(sysm.d) (the
+    identity holds for any D, SURVEY §8(c) "Any A, D").  Returns e_pred [R, n]
+    (original ordering)."""
     B = sysm.b if B is None else B
     A = _dense(sysm)
-    d = np.asarray(sysm.d, dtype=np.float64)
+    Dm = np.diag(np.asarray(sysm.d, dtype=np.float64)) if Dm is None else np.asarray(Dm, np.float64)
     LU, piv, st = lu_partial_pivot(A)
     if st:
         raise ValueError("singular A")
 
     def M(v):
-        return lu_pp_solve(LU, piv, d * v)
+        return lu_pp_solve(LU, piv, Dm @ v)
 
     pairs = []
     for s in mags:
-        fp = lu_partial_pivot(A + float(s) * np.diag(d))
-        fm = lu_partial_pivot(A - float(s) * np.diag(d))
+        fp = lu_partial_pivot(A + float(s) * Dm)
+        fm = lu_partial_pivot(A - float(s) * Dm)
         if fp[2] or fm[2]:
             raise ValueError(f"singular A +- {s} D")
         pairs.append((float(s), fp, fm))
