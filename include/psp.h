@@ -151,11 +151,26 @@ psp_status psp_destroy(psp_handle h);
  *                         global area and reloaded before their next use):
  *                         2 CTAs x 7 warps per SM instead of 1 x 7-8; 1: always (when a
  *                         launch fits); 2: never.  Bitwise-neutral.
+ *  PSP_OPT_PATH           PSP_PATH_SPARSE (default) or PSP_PATH_DENSE: which kernels the
+ *                         next factorisations run (may change at any time; the
+ *                         solve follows the last factorisation).  DENSE is the paper's own
+ *                         formulation (a dense no-pivot getrf/trsm per
+ *                         perturbed copy, "getrf_batched! / trsm_batched!"): every lane's
+ *                         P (A + eps_k D) P^T as a dense matrix (n padded to a multiple of
+ *                         32, 8 * N^2 bytes per lane), right-looking blocked elimination in
+ *                         32-column panels with the trailing updates on the FP64 tensor
+ *                         path (DMMA), and dense triangular solves.  Same pivot order
+ *                         (perm; PSP_ORDER_NATURAL = the paper-replica mode), statuses,
+ *                         tolerance and X layout as the sparse path; the arithmetic is
+ *                         blocked (NOT bitwise the canonical order, R19).  Needs
+ *                         N x 33 x 8 bytes <= 227 KB of shared memory (n <= 864).  The
+ *                         only path for a dense D (psp_set_perturbation_matrix).
  * Errors: ARG (STATE: PSP_OPT_PHASE_EVENTS on a host-only handle). */
+enum { PSP_PATH_SPARSE = 0, PSP_PATH_DENSE = 1 };
 enum { PSP_OPT_FACTOR_GROUPS = 1, PSP_OPT_FACTOR_WARPS = 2, PSP_OPT_FACTOR_LANES = 3,
        PSP_OPT_FACTOR_SLAB_WARPS = 4, PSP_OPT_FACTOR_PAIRS = 5, PSP_OPT_FACTOR_TMEM = 6,
        PSP_OPT_SOLVE_TMEM = 7, PSP_OPT_PHASE_EVENTS = 8, PSP_OPT_GROWTH = 9,
-       PSP_OPT_COOP = 10, PSP_OPT_FACTOR_SPILL = 11 };
+       PSP_OPT_COOP = 10, PSP_OPT_FACTOR_SPILL = 11, PSP_OPT_PATH = 12 };
 psp_status psp_set_option(psp_handle h, int32_t option, int64_t value);
 
 /* Rebind the handle to another stream of the same device.  Synchronises the old stream
@@ -270,8 +285,9 @@ enum { PSP_KERNEL_NONE = 0,
        PSP_KERNEL_COOP = 1,        /* cooperative small-batch kernels (CTA per system)      */
        PSP_KERNEL_BATCH = 2,       /* batch kernels, slots in shared (or global) memory      */
        PSP_KERNEL_BATCH_TMEM = 3,  /* batch kernels, slots in tensor memory + shared memory  */
-       PSP_KERNEL_BATCH_SPILL = 4  /* batch factor, capacity-planned slots (TMEM + shared)
+       PSP_KERNEL_BATCH_SPILL = 4, /* batch factor, capacity-planned slots (TMEM + shared)
                                       with idle entries spilled to global memory            */
+       PSP_KERNEL_DENSE = 5        /* dense path (PSP_OPT_PATH): blocked LU / solves, DMMA   */
 };
 psp_status psp_get_last_kernels(psp_handle h, int32_t* kernels_h);
 
@@ -285,6 +301,23 @@ psp_status psp_get_solutions(psp_handle h, double* X);
  * u_{p i} for the same i).  The row sets are those of the symbolic factorisation of
  * pattern(A + A^T + I) in the order of psp_get_symbolic_info's perm.  Errors: ARG, STATE. */
 psp_status psp_get_factor(psp_handle h, int32_t k, double* vals_h);
+
+/* Dense path only: copy lane k's dense factor to the host (synchronises): lu_h[n*n]
+ * row-major in the PERMUTED order, strict lower part = L (unit diagonal implied), upper
+ * part with the diagonal = U (the layout of a LAPACK-style getrf without pivots, row-major).
+ * Errors: ARG, STATE (no dense factorisation), CUDA. */
+psp_status psp_get_dense_factor(psp_handle h, int32_t k, double* lu_h);
+
+/* A general perturbation matrix D (footnote P:L72; "all entries of
+ * the perturbation matrix ... normally distributed"): lane k then factors
+ * A + eps_k * D entry by entry (a_ij + (eps_k * D_ij), a_ij = 0 outside the pattern) instead
+ * of A + eps_k * diag(d).  D_h: n x n row-major, ORIGINAL ordering, finite (host; copied,
+ * permuted, 8 n^2 bytes on the device); NULL returns to the diagonal d of
+ * psp_set_perturbations.  A dense D has no shared sparse pattern: factorisations need
+ * PSP_OPT_PATH = PSP_PATH_DENSE (else PSP_ERR_UNSUPPORTED).  psp_estimate_rho uses it.
+ * Invalidates the factorisation.  Errors: ARG, STATE (analyse first), UNSUPPORTED
+ * (host-only handle), ALLOC, CUDA. */
+psp_status psp_set_perturbation_matrix(psp_handle h, const double* D_h);
 
 /* Recombination weights (Remark 2 / Eq. (13), with the pair average of
  * Eq. (avg_hats), folded in: weight beta_j / 2 on each sign).  CSR over

@@ -21,6 +21,7 @@
 
 #include "../../include/psp.h"
 #include "psp_internal.h"
+#include "psp_dense.h"
 #include "psp_plan.h"
 
 using psp::DevicePlan;
@@ -163,6 +164,20 @@ struct psp_ctx {
   int32_t w_uni = 0;            // L when weight row w is lanes [w*L, w*L+L) for every w
   bool recovered = false;
 
+  // --- dense path (PSP_OPT_PATH = PSP_PATH_DENSE, psp_dense.cu): the paper's dense
+  // no-pivot getrf/trsm formulation on DMMA; also the only path for a dense D ---
+  int64_t opt_path = 0;
+  int32_t dense_N = 0;                 // n padded to a multiple of 32
+  const int32_t* drp_d = nullptr;      // plan buffers: permuted CSR of A (row_ptr, col, src)
+  const int32_t* dci_d = nullptr;
+  const int32_t* dsrc_d = nullptr;
+  bool dense_configured = false;
+  DevBuf Md_d;                         // [K][N][N] dense factors
+  DevBuf Dp_d;                         // P D P^T (n x n) when a dense D is set
+  bool dense_D = false;
+  std::vector<double> D_host;          // the dense D, original ordering (psp_estimate_rho)
+  bool dense_factored = false;         // the last factorisation ran the dense path
+
   // kernels of the last numeric calls (psp_get_last_kernels)
   int32_t last_factor = 0, last_factor_aug = 0, last_solve = 0, last_solve_fwd = 0;
 
@@ -233,6 +248,12 @@ static void release_plan(psp_ctx* h) {
   h->plan = DevicePlan{};
   h->isdiag_d = nullptr;
   h->rowptr_d = h->colidx_d = nullptr;
+  h->drp_d = h->dci_d = h->dsrc_d = nullptr;
+  h->dense_N = 0;
+  h->dense_configured = false;
+  h->Dp_d.release();
+  h->dense_D = false;
+  h->D_host.clear();
 }
 
 static void reset_numeric(psp_ctx* h) {
@@ -252,6 +273,8 @@ static void reset_numeric(psp_ctx* h) {
   h->w_uni = 0;
   h->growth_d.release();
   h->offmax_d.release();
+  h->Md_d.release();
+  h->dense_factored = false;
   h->K = h->K_pad = h->R = h->W = 0;
   h->factored = h->solved = h->recovered = h->growth_valid = false;
 }
@@ -382,6 +405,11 @@ psp_status psp_set_option(psp_handle h, int32_t option, int64_t value) {
       if (value != 0 && value != 1 && value != 2)
         return fail(h, PSP_ERR_ARG, "PSP_OPT_FACTOR_SLAB_WARPS must be 0, 1 or 2");
       h->opt_slab_warps = value;
+      return PSP_OK;
+    case PSP_OPT_PATH:
+      if (value != PSP_PATH_SPARSE && value != PSP_PATH_DENSE)
+        return fail(h, PSP_ERR_ARG, "PSP_OPT_PATH must be PSP_PATH_SPARSE or PSP_PATH_DENSE");
+      h->opt_path = value;
       return PSP_OK;
     case PSP_OPT_FACTOR_WARPS:
       if (value < 0 || value > psp::kMaxWarpsCta)
@@ -782,6 +810,28 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
     auto store = [](const psp::LaunchInfo& li) { return li.f_tmem ? 2 : (li.f_pend_smem ? 1 : 0); };
     h->aug_fast = h->aug_ok && store(la) == store(h->launch);
   }
+  if (!host_only) {   // the dense path's permuted CSR: row i of P A P^T, ascending columns
+    std::vector<int32_t> ip(n), drp(n + 1, 0), dci, dsrc;
+    for (int32_t i = 0; i < n; ++i) ip[perm[i]] = i;
+    dci.reserve(nnzA);
+    dsrc.reserve(nnzA);
+    std::vector<std::pair<int32_t, int32_t>> row;
+    for (int32_t i = 0; i < n; ++i) {
+      const int32_t o = perm[i];
+      row.clear();
+      for (int32_t q = row_ptr_h[o]; q < row_ptr_h[o + 1]; ++q) row.emplace_back(ip[col_idx_h[q]], q);
+      std::sort(row.begin(), row.end());
+      for (auto& e : row) {
+        dci.push_back(e.first);
+        dsrc.push_back(e.second);
+      }
+      drp[i + 1] = (int32_t)dci.size();
+    }
+    if ((s = upload(h, drp, &h->drp_d))) return s;
+    if ((s = upload(h, dci, &h->dci_d))) return s;
+    if ((s = upload(h, dsrc, &h->dsrc_d))) return s;
+    h->dense_N = psp::dense_padded_order(n);
+  }
   h->plan = P;
   h->perm = perm;
   h->n = n;
@@ -921,12 +971,96 @@ static bool use_spill(psp_ctx* h, bool aug) {
   return (int64_t)(h->K_pad / kBlock) > round;
 }
 
+// Dense path (psp_dense.cu): K padded N x N factors, one CTA per lane.
+static psp_status dense_factor(psp_handle h, const double* A_vals, double pivot_tol,
+                               int32_t* lane_status) {
+  if (h->growth) return fail(h, PSP_ERR_UNSUPPORTED, "PSP_OPT_GROWTH is a sparse-path pass");
+  const int32_t N = h->dense_N;
+  cudaSetDevice(h->device);
+  psp_status s;
+  const size_t need = sizeof(double) * (size_t)h->K * N * N;
+  if (h->Md_d.bytes < need) {
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    if ((s = ensure(h, h->Md_d, need))) return s;
+  }
+  if (!h->dense_configured) {
+    if (psp::dense_lu_smem(N) > (size_t)(227 * 1024))
+      return fail(h, PSP_ERR_UNSUPPORTED, "dense path: n = %d exceeds the panel's shared memory", h->n);
+    CUDA_TRY(h, psp::configure_dense(N));
+    h->dense_configured = true;
+  }
+  const double* tol_dev = nullptr;
+  if (pivot_tol <= 0) {
+    CUDA_TRY(h, psp::launch_pivot_tol(h->plan, A_vals, (double*)h->tol_d.p, h->stream));
+    tol_dev = (const double*)h->tol_d.p;
+  }
+  psp::DenseArgs a;
+  a.n = h->n;
+  a.N = N;
+  a.rp = h->drp_d;
+  a.ci = h->dci_d;
+  a.src = h->dsrc_d;
+  a.A = A_vals;
+  a.eps = (const double*)h->eps_d.p;
+  a.dperm = (const double*)h->dperm_d.p;
+  a.Dp = h->dense_D ? (const double*)h->Dp_d.p : nullptr;
+  a.tol_dev = tol_dev;
+  a.tol_value = pivot_tol;
+  a.M = (double*)h->Md_d.p;
+  a.status = (int32_t*)h->status_d.p;
+  if (h->phase_events) {
+    if ((s = phase_mark(h, h->fev, h->nf))) return s;
+  }
+  h->last_factor = PSP_KERNEL_DENSE;
+  h->last_factor_aug = 0;
+  CUDA_TRY(h, psp::launch_dense_lu(a, h->K, h->stream));
+  if (h->phase_events) {
+    if ((s = phase_mark(h, h->fev, h->nf))) return s;
+  }
+  h->growth_valid = false;
+  if (lane_status)
+    CUDA_TRY(h, cudaMemcpyAsync(lane_status, h->status_d.p, sizeof(int32_t) * h->K,
+                                cudaMemcpyDeviceToDevice, h->stream));
+  h->factored = true;
+  h->dense_factored = true;
+  h->solved = h->recovered = false;
+  return PSP_OK;
+}
+
+static psp_status dense_solve(psp_handle h, int32_t R, const double* B, int64_t ldb) {
+  psp_status s;
+  if (h->phase_events) {
+    if ((s = phase_mark(h, h->sev, h->ns))) return s;
+  }
+  psp::DenseSolveArgs a;
+  a.n = h->n;
+  a.N = h->dense_N;
+  a.R = R;
+  a.ldb = ldb;
+  a.perm = h->plan.perm;
+  a.M = (const double*)h->Md_d.p;
+  a.B = B;
+  a.X = (double*)h->X_d.p;
+  h->last_solve = PSP_KERNEL_DENSE;
+  h->last_solve_fwd = 1;
+  CUDA_TRY(h, psp::launch_dense_solve(a, h->K, h->stream));
+  if (h->phase_events) {
+    if ((s = phase_mark(h, h->sev, h->ns))) return s;
+  }
+  h->R = R;
+  h->solved = true;
+  return PSP_OK;
+}
+
 static psp_status factor_impl(psp_handle h, const double* A_vals, double pivot_tol,
                               int32_t* lane_status, bool aug, const double* b) {
   if (!h) return PSP_ERR_ARG;
   if (!h->analysed || h->K == 0) return fail(h, PSP_ERR_STATE, "set_perturbations first");
   if (!A_vals) return fail(h, PSP_ERR_ARG, "A_vals required");
   if (!(pivot_tol == pivot_tol)) return fail(h, PSP_ERR_ARG, "pivot_tol is NaN");
+  if (h->opt_path == PSP_PATH_DENSE) return dense_factor(h, A_vals, pivot_tol, lane_status);
+  if (h->dense_D)
+    return fail(h, PSP_ERR_UNSUPPORTED, "a dense D needs the dense path (PSP_OPT_PATH = PSP_PATH_DENSE)");
   const bool spill = !use_coop(h) && use_spill(h, aug);
   const DevicePlan& P = spill ? (aug ? h->plan_spill_aug : h->plan_spill) : (aug ? h->plan_aug : h->plan);
   const psp::LaunchInfo& LI = spill ? (aug ? h->launch_spill_aug : h->launch_spill)
@@ -1004,6 +1138,7 @@ static psp_status factor_impl(psp_handle h, const double* A_vals, double pivot_t
     CUDA_TRY(h, cudaMemcpyAsync(lane_status, h->status_d.p, sizeof(int32_t) * h->K,
                                 cudaMemcpyDeviceToDevice, h->stream));
   h->factored = true;
+  h->dense_factored = false;
   h->solved = h->recovered = false;
   return PSP_OK;
 }
@@ -1031,6 +1166,10 @@ psp_status psp_factor_solve_batch(psp_handle h, const double* A_vals, const doub
   if (!h) return PSP_ERR_ARG;
   if (!b) return fail(h, PSP_ERR_ARG, "b required");
   psp_status s;
+  if (h->analysed && h->opt_path == PSP_PATH_DENSE) {
+    if ((s = factor_impl(h, A_vals, pivot_tol, lane_status, false, nullptr))) return s;
+    return psp_solve_batch(h, 1, b, h->n);
+  }
   const bool fuse = h->analysed && !use_coop(h) && (use_spill(h, true) || h->aug_fast);
   if (h->analysed && !fuse) {   // the two calls (bitwise the same)
     if ((s = factor_impl(h, A_vals, pivot_tol, lane_status, false, nullptr))) return s;
@@ -1066,6 +1205,7 @@ psp_status psp_solve_batch(psp_handle h, int32_t R, const double* B, int64_t ldb
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     if ((s = ensure(h, h->X_d, need))) return s;
   }
+  if (h->dense_factored) return dense_solve(h, R, B, ldb);
   if ((s = solve_scratch(h, R))) return s;
   if (h->phase_events) {
     if ((s = phase_mark(h, h->sev, h->ns))) return s;
@@ -1120,7 +1260,15 @@ psp_status psp_estimate_rho(psp_handle h, int32_t w, int32_t max_iter, double rt
   double rho = 0.0;
   int32_t it = 0, conv = 0;
   for (it = 1; it <= max_iter; ++it) {
-    for (int32_t i = 0; i < n; ++i) r[i] = h->d_host[i] * v[i];   // r = D v
+    if (h->dense_D) {   // r = D v (dense D, original ordering; long double row sums)
+      for (int32_t i = 0; i < n; ++i) {
+        long double acc = 0;
+        for (int32_t j = 0; j < n; ++j) acc += (long double)h->D_host[(size_t)i * n + j] * v[j];
+        r[i] = (double)acc;
+      }
+    } else {
+      for (int32_t i = 0; i < n; ++i) r[i] = h->d_host[i] * v[i];   // r = D v
+    }
     CUDA_TRY(h, cudaMemcpyAsync(h->rho_r_d.p, r.data(), sizeof(double) * n, cudaMemcpyHostToDevice,
                                 h->stream));
     if ((s = psp_solve_batch(h, 1, (const double*)h->rho_r_d.p, n))) return s;
@@ -1196,11 +1344,58 @@ psp_status psp_get_factor(psp_handle h, int32_t k, double* vals_h) {
   if (!h || !vals_h) return PSP_ERR_ARG;
   if (!h->factored) return fail(h, PSP_ERR_STATE, "factor_batch first");
   if (k < 0 || k >= h->K) return fail(h, PSP_ERR_ARG, "lane %d out of range", k);
+  if (h->dense_factored)
+    return fail(h, PSP_ERR_UNSUPPORTED, "dense factorisation: use psp_get_dense_factor");
   const int L = kBlock / h->launch.f_groups * h->launch.f_lanes;
   const double* src = (const double*)h->V_d.p + (size_t)(k / L) * h->nnz_LU * L + (k % L);
   CUDA_TRY(h, cudaMemcpy2DAsync(vals_h, sizeof(double), src, sizeof(double) * L, sizeof(double),
                                 (size_t)h->nnz_LU, cudaMemcpyDeviceToHost, h->stream));
   CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  return PSP_OK;
+}
+
+psp_status psp_get_dense_factor(psp_handle h, int32_t k, double* lu_h) {
+  if (!h || !lu_h) return PSP_ERR_ARG;
+  if (!h->factored || !h->dense_factored) return fail(h, PSP_ERR_STATE, "dense factor_batch first");
+  if (k < 0 || k >= h->K) return fail(h, PSP_ERR_ARG, "lane %d out of range", k);
+  const int32_t N = h->dense_N;
+  cudaSetDevice(h->device);
+  const double* src = (const double*)h->Md_d.p + (size_t)k * N * N;
+  CUDA_TRY(h, cudaMemcpy2DAsync(lu_h, sizeof(double) * h->n, src, sizeof(double) * N,
+                                sizeof(double) * h->n, (size_t)h->n, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  return PSP_OK;
+}
+
+psp_status psp_set_perturbation_matrix(psp_handle h, const double* D_h) {
+  if (!h) return PSP_ERR_ARG;
+  if (h->device < 0) return fail(h, PSP_ERR_UNSUPPORTED, "host-only handle (device < 0)");
+  if (!h->analysed) return fail(h, PSP_ERR_STATE, "psp_symbolic_analyse first");
+  cudaSetDevice(h->device);
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  if (!D_h) {
+    h->Dp_d.release();
+    h->D_host.clear();
+    h->dense_D = false;
+    h->factored = h->solved = h->recovered = false;
+    return PSP_OK;
+  }
+  const int32_t n = h->n;
+  std::vector<double> Dp((size_t)n * n);
+  for (int32_t i = 0; i < n; ++i) {
+    const double* row = D_h + (size_t)h->perm[i] * n;
+    for (int32_t j = 0; j < n; ++j) {
+      const double v = row[h->perm[j]];
+      if (!std::isfinite(v)) return fail(h, PSP_ERR_ARG, "D has a non-finite entry");
+      Dp[(size_t)i * n + j] = v;
+    }
+  }
+  psp_status s;
+  if ((s = ensure(h, h->Dp_d, sizeof(double) * Dp.size()))) return s;
+  CUDA_TRY(h, cudaMemcpy(h->Dp_d.p, Dp.data(), sizeof(double) * Dp.size(), cudaMemcpyHostToDevice));
+  h->D_host.assign(D_h, D_h + (size_t)n * n);
+  h->dense_D = true;
+  h->factored = h->solved = h->recovered = false;
   return PSP_OK;
 }
 

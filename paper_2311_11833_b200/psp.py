@@ -28,11 +28,13 @@ EXPORTS = ["psp_create", "psp_destroy", "psp_set_stream", "psp_status_string",
            "psp_synchronize", "psp_ladder_weights", "psp_set_option", "psp_get_factor", "psp_residual",
            "psp_rescale_failed_rows", "psp_get_perturbations", "psp_get_last_kernels",
            "psp_get_unique_id", "psp_comm_init", "psp_set_perturbations_shard", "psp_shard_weights",
-           "psp_set_weights_dense", "psp_recover_reduce"]
-KERNEL = {0: "none", 1: "coop", 2: "batch", 3: "batch_tmem", 4: "batch_spill"}
+           "psp_set_weights_dense", "psp_recover_reduce", "psp_get_dense_factor",
+           "psp_set_perturbation_matrix"]
+KERNEL = {0: "none", 1: "coop", 2: "batch", 3: "batch_tmem", 4: "batch_spill", 5: "dense"}
+PATH = {"sparse": 0, "dense": 1}
 OPT = {"factor_groups": 1, "factor_warps": 2, "factor_lanes": 3, "factor_slab_warps": 4,
        "factor_pairs": 5, "factor_tmem": 6, "solve_tmem": 7, "phase_events": 8, "growth": 9, "coop": 10,
-       "factor_spill": 11}
+       "factor_spill": 11, "path": 12}
 
 
 class SymbolicInfo(ctypes.Structure):
@@ -105,6 +107,8 @@ def lib():
             "psp_shard_weights": [I32, P, I32, I32, I32, P, P, P, P],
             "psp_set_weights_dense": [P, I32, P],
             "psp_recover_reduce": [P, P, I32],
+            "psp_get_dense_factor": [P, I32, P],
+            "psp_set_perturbation_matrix": [P, P],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -168,7 +172,26 @@ class Solver:
 
     # --- C-ABI wrappers ------------------------------------------------------
     def psp_set_option(self, name, value):
+        if name == "path" and isinstance(value, str):
+            value = PATH[value]
         self._check(lib().psp_set_option(self.h, OPT[name], int(value)))
+
+    def psp_set_perturbation_matrix(self, D):
+        """A general n x n perturbation matrix (host array, original ordering), or None to
+        return to the diagonal d of psp_set_perturbations (include/psp.h)."""
+        if D is None:
+            self._check(lib().psp_set_perturbation_matrix(self.h, None))
+            return
+        Dm = np.ascontiguousarray(D, dtype=np.float64)
+        if Dm.shape != (self.n, self.n):
+            raise ValueError("D must be n x n")
+        self._check(lib().psp_set_perturbation_matrix(self.h, _np_ptr(Dm)))
+
+    def psp_get_dense_factor(self, k):
+        """Lane k's dense factor (host numpy n x n, permuted order; L strict lower, U upper)."""
+        out = np.empty((self.n, self.n), dtype=np.float64)
+        self._check(lib().psp_get_dense_factor(self.h, int(k), _np_ptr(out)))
+        return out
 
     def psp_symbolic_analyse(self, n, row_ptr, col_idx, ordering="mindeg", user_perm=None, first_node=-1):
         rp = np.ascontiguousarray(row_ptr, dtype=np.int32)
