@@ -790,7 +790,7 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
       Pc.f_npatch = (int32_t)H.f_patch_pos.size();
       Pc.f_gspill = H.f_gspill;
       psp::LaunchInfo lc = h->launch;
-      if (!psp::choose_launch_spill(Pc, lc, 0)) continue;
+      if (!psp::choose_launch_spill(Pc, lc, (int)h->opt_warps)) continue;
       if (!host_only) {
         if ((s = upload(h, H.f_stream, &Pc.f_stream))) return s;
         if ((s = upload(h, H.f_patch_pos, &Pc.f_patch_pos))) return s;

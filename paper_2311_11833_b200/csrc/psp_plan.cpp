@@ -521,18 +521,38 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
   // a capacity, a pivot whose block + consumed entries exceed it is SPLIT into step A
   // (pivot record: L column and U row read into scratch, consumed entries die) and step B
   // (its births in BIRTH records, then UPDATE records): the large-pivot path.
-  std::vector<int32_t> stepA(n, -1), stepB(n, -1);
+  // Step B is itself split into row chunks of rpc[p] rows (one step each: the chunk's
+  // block rows are all the step needs resident), so a capacity below a whole update block
+  // (c x cu entries) stays feasible: a chunk needs rpc x cu slots.
+  std::vector<int32_t> stepA(n, -1), stepB(n, -1), rpc(n, 0);
   std::vector<char> split(n, 0);
   int32_t n_steps = 0;
   for (int32_t p = 0; p < n; ++p) {
     split[p] = capped && !paired[p] && need_of(p) > C;
     stepA[p] = n_steps++;
-    stepB[p] = split[p] ? n_steps++ : stepA[p];
+    if (split[p]) {
+      const int32_t c = (int32_t)lcol[p].size(), cu = c + (aug ? 1 : 0);
+      rpc[p] = std::max<int32_t>(1, std::min<int32_t>(c, C / std::max<int32_t>(1, cu)));
+      stepB[p] = n_steps;
+      n_steps += (c + rpc[p] - 1) / rpc[p];
+    } else {
+      stepB[p] = stepA[p];
+    }
     if (paired[p]) {
       stepA[p + 1] = stepB[p + 1] = stepA[p];
       ++p;
     }
   }
+  // the step of row a of split pivot p's update block
+  auto step_row = [&](int32_t p, int32_t a) { return split[p] ? stepB[p] + a / rpc[p] : stepB[p]; };
+  // the block entries of rows [a0, a1) of pivot p's update (+ the right-hand side column)
+  auto block_rows = [&](int32_t p, int32_t a0, int32_t a1, std::vector<int32_t>& u) {
+    const auto& L = lcol[p];
+    for (int32_t a = a0; a < a1; ++a) {
+      for (int32_t b : L) u.push_back(entry(L[a], b));
+      if (aug) u.push_back(entry_b(L[a]));
+    }
+  };
   P.c_scr_need = 0;
   for (int32_t p = 0; p < n; ++p) {
     const int32_t cu = (int32_t)lcol[p].size() + (aug ? 1 : 0);
@@ -547,7 +567,13 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
     for (int32_t p = 0; p < n; ++p) {
       if (p > 0 && paired[p - 1] && stepA[p] == stepA[p - 1]) continue;   // q of a pair
       consumed_of(p, uses[stepA[p]]);
-      block_of(p, uses[stepB[p]]);
+      if (split[p]) {
+        const int32_t c = (int32_t)lcol[p].size();
+        for (int32_t a0 = 0; a0 < c; a0 += rpc[p])
+          block_rows(p, a0, std::min(c, a0 + rpc[p]), uses[step_row(p, a0)]);
+      } else {
+        block_of(p, uses[stepB[p]]);
+      }
     }
     for (auto& u : uses) {
       std::sort(u.begin(), u.end());
@@ -840,30 +866,46 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
     push(std::move(r), std::move(pt));
     if (paired[p]) ++p;   // q's work is in p's record
     if (!fused) {
-      if (sp) {   // step B: make room, reload, births, then the update rows
-        cur_step = stepB[p];
-        emit_moves(kRecSpill, spill_at[cur_step]);
-        emit_moves(kRecReload, reload_at[cur_step]);
-        size_t zd = 0, zo = 0;
-        birth_records(bdB, boB, zd, zo, 20);
-        if (zd < bdB.size() || zo < boB.size()) {   // the rest (fits one record)
-          std::vector<int32_t> b = {(int32_t)(kRecBirth << 28), 0, 0, 0, 0, 0, 0, 0};
-          std::vector<std::pair<int32_t, int32_t>> pt2;
-          int32_t nd = 0, no = 0;
-          while (zd < bdB.size()) birth(b, pt2, bdB[zd++]), ++nd;
-          while (zo < boB.size()) birth(b, pt2, boB[zo++]), ++no;
-          while (no % 4) b.insert(b.end(), {dummy_slot, 0, 0, 0}), ++no;
-          b[2] = nd;
-          b[3] = no;
-          push(std::move(b), std::move(pt2));
-        }
-      }
       const int32_t rows_per = std::max<int32_t>(1, (int32_t)((kMaxRec - 8) / ws));
-      for (int32_t a0 = 0; a0 < c; a0 += rows_per) {
-        const int32_t na = std::min(rows_per, c - a0);
-        std::vector<int32_t> u = {(int32_t)((kRecUpdate << 28) | (uint32_t)c), a0, na, ws, 0, 0, 0, 0};
-        for (int32_t a = a0; a < a0 + na; ++a) row(u, a);
-        push(std::move(u), {});
+      auto updates = [&](int32_t r0, int32_t r1) {
+        for (int32_t a0 = r0; a0 < r1; a0 += rows_per) {
+          const int32_t na = std::min(rows_per, r1 - a0);
+          std::vector<int32_t> u = {(int32_t)((kRecUpdate << 28) | (uint32_t)c), a0, na, ws, 0, 0, 0, 0};
+          for (int32_t a = a0; a < a0 + na; ++a) row(u, a);
+          push(std::move(u), {});
+        }
+      };
+      if (sp) {   // step B, chunk by chunk: make room, reload, the chunk's births, its rows
+        // (the block's births by row: entry (L[a], .) belongs to row a)
+        std::vector<int32_t> row_of(n + 1, -1);
+        for (int32_t a = 0; a < c; ++a) row_of[L[a]] = a;
+        for (int32_t r0 = 0; r0 < c; r0 += rpc[p]) {
+          const int32_t r1 = std::min(c, r0 + rpc[p]);
+          cur_step = step_row(p, r0);
+          emit_moves(kRecSpill, spill_at[cur_step]);
+          emit_moves(kRecReload, reload_at[cur_step]);
+          std::vector<int32_t> cd, co;
+          for (int32_t e : bdB)
+            if (row_of[ent_i[e]] >= r0 && row_of[ent_i[e]] < r1) cd.push_back(e);
+          for (int32_t e : boB)
+            if (row_of[ent_i[e]] >= r0 && row_of[ent_i[e]] < r1) co.push_back(e);
+          size_t zd = 0, zo = 0;
+          birth_records(cd, co, zd, zo, 20);
+          if (zd < cd.size() || zo < co.size()) {   // the rest (fits one record)
+            std::vector<int32_t> b = {(int32_t)(kRecBirth << 28), 0, 0, 0, 0, 0, 0, 0};
+            std::vector<std::pair<int32_t, int32_t>> pt2;
+            int32_t nd = 0, no = 0;
+            while (zd < cd.size()) birth(b, pt2, cd[zd++]), ++nd;
+            while (zo < co.size()) birth(b, pt2, co[zo++]), ++no;
+            while (no % 4) b.insert(b.end(), {dummy_slot, 0, 0, 0}), ++no;
+            b[2] = nd;
+            b[3] = no;
+            push(std::move(b), std::move(pt2));
+          }
+          updates(r0, r1);
+        }
+      } else {
+        updates(0, c);
       }
     }
   }
