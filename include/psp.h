@@ -151,6 +151,13 @@ psp_status psp_destroy(psp_handle h);
  *                         global area and reloaded before their next use):
  *                         2 CTAs x 7 warps per SM instead of 1 x 7-8; 1: always (when a
  *                         launch fits); 2: never.  Bitwise-neutral.
+ *  PSP_OPT_COOP_GLOBAL    0 (default): automatic -- when the cooperative kernels' factor
+ *                         image does not fit shared memory (large n, e.g. SURVEY §8(d)
+ *                         configs 3-4) and K <= 8 x the SM count, factor and solve with the
+ *                         global-memory level-scheduled kernels (one CTA per system, the
+ *                         factor image lane-major in the handle's factor storage, the same
+ *                         etree-level schedule: bitwise the batch kernels); 1: always (when
+ *                         built: set before psp_symbolic_analyse); 2: never.  Bitwise-neutral.
  *  PSP_OPT_PATH           PSP_PATH_SPARSE (default) or PSP_PATH_DENSE: which kernels the
  *                         next factorisations run (may change at any time; the
  *                         solve follows the last factorisation).  DENSE is the paper's own
@@ -170,7 +177,7 @@ enum { PSP_PATH_SPARSE = 0, PSP_PATH_DENSE = 1 };
 enum { PSP_OPT_FACTOR_GROUPS = 1, PSP_OPT_FACTOR_WARPS = 2, PSP_OPT_FACTOR_LANES = 3,
        PSP_OPT_FACTOR_SLAB_WARPS = 4, PSP_OPT_FACTOR_PAIRS = 5, PSP_OPT_FACTOR_TMEM = 6,
        PSP_OPT_SOLVE_TMEM = 7, PSP_OPT_PHASE_EVENTS = 8, PSP_OPT_GROWTH = 9,
-       PSP_OPT_COOP = 10, PSP_OPT_FACTOR_SPILL = 11, PSP_OPT_PATH = 12 };
+       PSP_OPT_COOP = 10, PSP_OPT_FACTOR_SPILL = 11, PSP_OPT_PATH = 12, PSP_OPT_COOP_GLOBAL = 13 };
 psp_status psp_set_option(psp_handle h, int32_t option, int64_t value);
 
 /* Rebind the handle to another stream of the same device.  Synchronises the old stream
@@ -287,7 +294,9 @@ enum { PSP_KERNEL_NONE = 0,
        PSP_KERNEL_BATCH_TMEM = 3,  /* batch kernels, slots in tensor memory + shared memory  */
        PSP_KERNEL_BATCH_SPILL = 4, /* batch factor, capacity-planned slots (TMEM + shared)
                                       with idle entries spilled to global memory            */
-       PSP_KERNEL_DENSE = 5        /* dense path (PSP_OPT_PATH): blocked LU / solves, DMMA   */
+       PSP_KERNEL_DENSE = 5,       /* dense path (PSP_OPT_PATH): blocked LU / solves, DMMA   */
+       PSP_KERNEL_COOP_GLOBAL = 6  /* level-scheduled CTA per system, factor image in global
+                                      memory (large n, PSP_OPT_COOP_GLOBAL)                  */
 };
 psp_status psp_get_last_kernels(psp_handle h, int32_t* kernels_h);
 

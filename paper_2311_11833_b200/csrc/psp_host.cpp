@@ -21,6 +21,7 @@
 
 #include "../../include/psp.h"
 #include "psp_internal.h"
+#include "psp_coopg.h"
 #include "psp_dense.h"
 #include "psp_plan.h"
 
@@ -100,6 +101,12 @@ struct psp_ctx {
   psp::CoopDev coop;
   bool coop_ok = false;
   int64_t opt_coop = 0;            // PSP_OPT_COOP: 0 automatic (K <= 8 * SMs), 1 on, 2 off
+  // level-scheduled kernels for large systems (CTA per system, factor image lane-major in
+  // V_d: psp_coopg.cu), used when the cooperative kernels' shared-memory image does not fit
+  psp::CoopGDev coopg;
+  bool coopg_ok = false;
+  int64_t opt_coopg = 0;           // PSP_OPT_COOP_GLOBAL: 0 automatic, 1 on, 2 off
+  bool coopg_factored = false;     // the last factorisation ran them (V_d is lane-major)
   // program of the augmented matrix [A | b] (psp_factor_solve_batch); its own slots,
   // stream and factor launch configuration, the rest shared with `plan`
   DevicePlan plan_aug;
@@ -378,6 +385,10 @@ psp_status psp_set_option(psp_handle h, int32_t option, int64_t value) {
     case PSP_OPT_COOP:
       if (value < 0 || value > 2) return fail(h, PSP_ERR_ARG, "PSP_OPT_COOP must be 0, 1 or 2");
       h->opt_coop = value;
+      return PSP_OK;
+    case PSP_OPT_COOP_GLOBAL:
+      if (value < 0 || value > 2) return fail(h, PSP_ERR_ARG, "PSP_OPT_COOP_GLOBAL must be 0, 1 or 2");
+      h->opt_coopg = value;
       return PSP_OK;
     case PSP_OPT_FACTOR_SPILL:
       if (value < 0 || value > 2) return fail(h, PSP_ERR_ARG, "PSP_OPT_FACTOR_SPILL must be 0, 1 or 2");
@@ -744,6 +755,47 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
       c = psp::CoopDev{};
     }
   }
+  h->coopg_ok = false;
+  h->coopg = psp::CoopGDev{};
+  if (!host_only && h->opt_coopg != 2 && (!h->coop_ok || h->opt_coopg == 1)) {
+    psp::CoopGDev& g = h->coopg;
+    auto pairs = [](const std::vector<int32_t>& x, const std::vector<int32_t>& y) {
+      std::vector<int2> v(x.size());
+      for (size_t q = 0; q < x.size(); ++q) v[q] = make_int2(x[q], y[q]);
+      return v;
+    };
+    auto heads = [](const std::vector<int32_t>& t, const std::vector<int32_t>& cptr) {
+      std::vector<int2> v(t.size() + 1);
+      for (size_t q = 0; q < t.size(); ++q) v[q] = make_int2(t[q], cptr[q]);
+      v[t.size()] = make_int2(0, cptr.back());   // sentinel: end of the last one
+      return v;
+    };
+    g.steps = CP.steps;
+    g.nnz_LU = HP.nnz_LU;
+    g.n = n;
+    if ((s = upload(h, CP.birth_src, &g.birth_src))) return s;
+    if ((s = upload(h, CP.birth_diag, &g.birth_diag))) return s;
+    if ((s = upload(h, CP.fa_ptr, &g.fa_ptr))) return s;
+    if ((s = upload(h, CP.fp_ptr, &g.fp_ptr))) return s;
+    if ((s = upload(h, CP.fb_ptr, &g.fb_ptr))) return s;
+    if ((s = upload(h, pairs(CP.fa_l, CP.fa_d), &g.fa))) return s;
+    if ((s = upload(h, pairs(CP.fp_d, CP.fp_p), &g.fp))) return s;
+    if ((s = upload(h, heads(CP.fb_t, CP.fb_cptr), &g.fbt))) return s;
+    if ((s = upload(h, pairs(CP.fb_l, CP.fb_u), &g.fbc))) return s;
+    if ((s = upload(h, CP.ya_ptr, &g.ya_ptr))) return s;
+    if ((s = upload(h, CP.xb_ptr, &g.xb_ptr))) return s;
+    if ((s = upload(h, heads(CP.ya_t, CP.ya_cptr), &g.yat))) return s;
+    if ((s = upload(h, pairs(CP.ya_l, CP.ya_p), &g.yac))) return s;
+    if ((s = upload(h, heads(CP.xb_r, CP.xb_cptr), &g.xbr))) return s;
+    if ((s = upload(h, CP.xb_d, &g.xbd))) return s;
+    if ((s = upload(h, pairs(CP.xb_u, CP.xb_k), &g.xbc))) return s;
+    if (psp::coopg_solve_smem(n) <= (size_t)(227 * 1024) && psp::configure_coopg(n) == cudaSuccess) {
+      h->coopg_ok = true;
+    } else {
+      cudaGetLastError();
+      g = psp::CoopGDev{};
+    }
+  }
   h->stm_ok = false;
   if (h->opt_solve_tmem == 0) {
     psp::LaunchInfo ls = h->launch;
@@ -947,6 +999,14 @@ static bool use_coop(psp_ctx* h, int32_t R = 1) {
   return h->opt_coop == 1 || (h->K <= 8 * h->n_sm && R <= 8);
 }
 
+// The global-memory level-scheduled kernels for this batch? (large systems whose factor
+// image does not fit shared memory, few systems: a CTA per system beats a thread per
+// lane; PSP_OPT_COOP_GLOBAL overrides)
+static bool use_coopg(psp_ctx* h) {
+  if (!h->coopg_ok || h->opt_coopg == 2 || use_coop(h)) return false;
+  return h->opt_coopg == 1 || h->K <= 8 * h->n_sm;
+}
+
 // Record the next event of a phase pool on the handle's stream (growing the pool).
 static psp_status phase_mark(psp_ctx* h, std::vector<cudaEvent_t>& pool, size_t& used) {
   if (used == pool.size()) {
@@ -1023,6 +1083,7 @@ static psp_status dense_factor(psp_handle h, const double* A_vals, double pivot_
                                 cudaMemcpyDeviceToDevice, h->stream));
   h->factored = true;
   h->dense_factored = true;
+  h->coopg_factored = false;
   h->solved = h->recovered = false;
   return PSP_OK;
 }
@@ -1052,6 +1113,68 @@ static psp_status dense_solve(psp_handle h, int32_t R, const double* B, int64_t 
   return PSP_OK;
 }
 
+// Global-memory level-scheduled factor (psp_coopg.cu): V_d holds lane-major images.
+static psp_status coopg_factor(psp_handle h, const double* A_vals, double pivot_tol,
+                               int32_t* lane_status) {
+  if (h->growth) return fail(h, PSP_ERR_UNSUPPORTED, "PSP_OPT_GROWTH reads the batch factor layout");
+  cudaSetDevice(h->device);
+  psp_status s;
+  psp::CoopGArgs a;
+  a.c = h->coopg;
+  a.A = A_vals;
+  a.eps = (const double*)h->eps_d.p;
+  a.dperm = (const double*)h->dperm_d.p;
+  if (pivot_tol <= 0) {
+    CUDA_TRY(h, psp::launch_pivot_tol(h->plan, A_vals, (double*)h->tol_d.p, h->stream));
+    a.tol_dev = (const double*)h->tol_d.p;
+  }
+  a.tol_value = pivot_tol;
+  a.W = (double*)h->V_d.p;   // (K_pad x nnz_LU doubles: the same bytes as the batch layout)
+  a.status = (int32_t*)h->status_d.p;
+  if (h->phase_events) {
+    if ((s = phase_mark(h, h->fev, h->nf))) return s;
+  }
+  h->last_factor = PSP_KERNEL_COOP_GLOBAL;
+  h->last_factor_aug = 0;
+  CUDA_TRY(h, psp::launch_coopg_factor(a, h->K, h->stream));
+  if (h->phase_events) {
+    if ((s = phase_mark(h, h->fev, h->nf))) return s;
+  }
+  h->growth_valid = false;
+  if (lane_status)
+    CUDA_TRY(h, cudaMemcpyAsync(lane_status, h->status_d.p, sizeof(int32_t) * h->K,
+                                cudaMemcpyDeviceToDevice, h->stream));
+  h->factored = true;
+  h->dense_factored = false;
+  h->coopg_factored = true;
+  h->solved = h->recovered = false;
+  return PSP_OK;
+}
+
+static psp_status coopg_solve(psp_handle h, int32_t R, const double* B, int64_t ldb) {
+  psp_status s;
+  if (h->phase_events) {
+    if ((s = phase_mark(h, h->sev, h->ns))) return s;
+  }
+  psp::CoopGSolveArgs a;
+  a.c = h->coopg;
+  a.perm = h->plan.perm;
+  a.W = (const double*)h->V_d.p;
+  a.B = B;
+  a.ldb = ldb;
+  a.R = R;
+  a.X = (double*)h->X_d.p;
+  h->last_solve = PSP_KERNEL_COOP_GLOBAL;
+  h->last_solve_fwd = 1;
+  CUDA_TRY(h, psp::launch_coopg_solve(a, h->K, h->stream));
+  if (h->phase_events) {
+    if ((s = phase_mark(h, h->sev, h->ns))) return s;
+  }
+  h->R = R;
+  h->solved = true;
+  return PSP_OK;
+}
+
 static psp_status factor_impl(psp_handle h, const double* A_vals, double pivot_tol,
                               int32_t* lane_status, bool aug, const double* b) {
   if (!h) return PSP_ERR_ARG;
@@ -1061,6 +1184,7 @@ static psp_status factor_impl(psp_handle h, const double* A_vals, double pivot_t
   if (h->opt_path == PSP_PATH_DENSE) return dense_factor(h, A_vals, pivot_tol, lane_status);
   if (h->dense_D)
     return fail(h, PSP_ERR_UNSUPPORTED, "a dense D needs the dense path (PSP_OPT_PATH = PSP_PATH_DENSE)");
+  if (use_coopg(h)) return coopg_factor(h, A_vals, pivot_tol, lane_status);
   const bool spill = !use_coop(h) && use_spill(h, aug);
   const DevicePlan& P = spill ? (aug ? h->plan_spill_aug : h->plan_spill) : (aug ? h->plan_aug : h->plan);
   const psp::LaunchInfo& LI = spill ? (aug ? h->launch_spill_aug : h->launch_spill)
@@ -1139,6 +1263,7 @@ static psp_status factor_impl(psp_handle h, const double* A_vals, double pivot_t
                                 cudaMemcpyDeviceToDevice, h->stream));
   h->factored = true;
   h->dense_factored = false;
+  h->coopg_factored = false;
   h->solved = h->recovered = false;
   return PSP_OK;
 }
@@ -1166,7 +1291,7 @@ psp_status psp_factor_solve_batch(psp_handle h, const double* A_vals, const doub
   if (!h) return PSP_ERR_ARG;
   if (!b) return fail(h, PSP_ERR_ARG, "b required");
   psp_status s;
-  if (h->analysed && h->opt_path == PSP_PATH_DENSE) {
+  if (h->analysed && (h->opt_path == PSP_PATH_DENSE || use_coopg(h))) {
     if ((s = factor_impl(h, A_vals, pivot_tol, lane_status, false, nullptr))) return s;
     return psp_solve_batch(h, 1, b, h->n);
   }
@@ -1206,6 +1331,7 @@ psp_status psp_solve_batch(psp_handle h, int32_t R, const double* B, int64_t ldb
     if ((s = ensure(h, h->X_d, need))) return s;
   }
   if (h->dense_factored) return dense_solve(h, R, B, ldb);
+  if (h->coopg_factored) return coopg_solve(h, R, B, ldb);
   if ((s = solve_scratch(h, R))) return s;
   if (h->phase_events) {
     if ((s = phase_mark(h, h->sev, h->ns))) return s;
@@ -1346,6 +1472,13 @@ psp_status psp_get_factor(psp_handle h, int32_t k, double* vals_h) {
   if (k < 0 || k >= h->K) return fail(h, PSP_ERR_ARG, "lane %d out of range", k);
   if (h->dense_factored)
     return fail(h, PSP_ERR_UNSUPPORTED, "dense factorisation: use psp_get_dense_factor");
+  if (h->coopg_factored) {   // lane-major images
+    cudaSetDevice(h->device);
+    CUDA_TRY(h, cudaMemcpyAsync(vals_h, (const double*)h->V_d.p + (size_t)k * h->nnz_LU,
+                                sizeof(double) * h->nnz_LU, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    return PSP_OK;
+  }
   const int L = kBlock / h->launch.f_groups * h->launch.f_lanes;
   const double* src = (const double*)h->V_d.p + (size_t)(k / L) * h->nnz_LU * L + (k % L);
   CUDA_TRY(h, cudaMemcpy2DAsync(vals_h, sizeof(double), src, sizeof(double) * L, sizeof(double),

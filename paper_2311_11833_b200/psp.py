@@ -30,11 +30,11 @@ EXPORTS = ["psp_create", "psp_destroy", "psp_set_stream", "psp_status_string",
            "psp_get_unique_id", "psp_comm_init", "psp_set_perturbations_shard", "psp_shard_weights",
            "psp_set_weights_dense", "psp_recover_reduce", "psp_get_dense_factor",
            "psp_set_perturbation_matrix"]
-KERNEL = {0: "none", 1: "coop", 2: "batch", 3: "batch_tmem", 4: "batch_spill", 5: "dense"}
+KERNEL = {0: "none", 1: "coop", 2: "batch", 3: "batch_tmem", 4: "batch_spill", 5: "dense", 6: "coop_global"}
 PATH = {"sparse": 0, "dense": 1}
 OPT = {"factor_groups": 1, "factor_warps": 2, "factor_lanes": 3, "factor_slab_warps": 4,
        "factor_pairs": 5, "factor_tmem": 6, "solve_tmem": 7, "phase_events": 8, "growth": 9, "coop": 10,
-       "factor_spill": 11, "path": 12}
+       "factor_spill": 11, "path": 12, "coop_global": 13}
 
 
 class SymbolicInfo(ctypes.Structure):
