@@ -251,6 +251,27 @@ psp_status psp_solve_batch(psp_handle h, int32_t R, const double* B, int64_t ldb
 psp_status psp_factor_solve_batch(psp_handle h, const double* A_vals, const double* b,
                                   double pivot_tol, int32_t* lane_status);
 
+/* Many Jacobians of one pattern in one launch (the Newton-Raphson steps /
+ * the 25 voltage starts of P:L302, P:L323 share J's sparsity pattern): the K lanes are split
+ * into n_jac equal contiguous groups (n_jac must divide K) and lane k factors
+ * A_j + eps_k D with j = k / (K / n_jac).  A_vals (device) holds n_jac value arrays of nnz_A
+ * entries back to back (CSR order of the analysed pattern).  pivot_tol <= 0 selects each
+ * Jacobian's own n * 2^-52 * ||A_j||_1.  Runs the kernels that take one CTA per system:
+ * the cooperative (K <= 8 x SMs, PSP_OPT_COOP), global-memory level-scheduled
+ * (PSP_OPT_COOP_GLOBAL) or dense (PSP_OPT_PATH) kernels -- the same arithmetic as
+ * psp_factor_batch, bitwise; else PSP_ERR_UNSUPPORTED (factor such batches per Jacobian
+ * with psp_factor_batch: values-only refactorisation).  n_jac = 1 is psp_factor_batch.
+ * Errors: ARG (n_jac does not divide K), STATE, UNSUPPORTED, ALLOC, CUDA. */
+psp_status psp_factor_batch_multi(psp_handle h, int32_t n_jac, const double* A_vals, double pivot_tol,
+                                  int32_t* lane_status);
+
+/* Solves after psp_factor_batch_multi with each Jacobian's own R right-hand sides: lane k
+ * (Jacobian j) solves for B + j * jac_stride (device; n x R column-major with leading
+ * dimension ldb, ORIGINAL ordering).  Solutions as psp_solve_batch.  Errors: ARG
+ * (jac_stride < (R - 1) ldb + n), STATE (no multi-Jacobian factorisation), UNSUPPORTED,
+ * ALLOC, CUDA. */
+psp_status psp_solve_batch_multi(psp_handle h, int32_t R, const double* B, int64_t ldb, int64_t jac_stride);
+
 /* Spectral radius rho(A^-1 D) by power iteration (Eq. (4)'s rho; the convergence
  * premise eps_c = m eps < 1 / rho of Theorem 1),
  * reusing the handle's factorisation: A^-1 r is applied as the recovered solution w of

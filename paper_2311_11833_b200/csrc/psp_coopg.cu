@@ -72,12 +72,14 @@ __global__ void __launch_bounds__(kCgThreads, 4) coopg_factor_kernel(const __gri
   double* __restrict__ v = a.W + (size_t)k * c.nnz_LU;
   if (tid == 0) st = INT_MAX;
   const double e = a.eps[k];
+  const int jac = a.mj.jac(k);
+  const double* __restrict__ A = a.A + (size_t)jac * a.mj.a_stride;
   for (int q = tid; q < c.nnz_LU; q += kCgThreads) {   // births (a + (eps d) on the diagonal)
     const int sidx = c.birth_src[q], d = c.birth_diag[q];
-    const double av = sidx >= 0 ? a.A[sidx] : 0.0;
+    const double av = sidx >= 0 ? A[sidx] : 0.0;
     v[q] = d >= 0 ? __dadd_rn(av, __dmul_rn(e, a.dperm[d])) : av;
   }
-  const double tol = a.tol_dev ? *a.tol_dev : a.tol_value;
+  const double tol = a.tol_dev ? a.tol_dev[jac] : a.tol_value;
   __syncthreads();
   for (int step = 0; step < c.steps; ++step) {
     for (int j = c.fp_ptr[step] + tid; j < c.fp_ptr[step + 1]; j += kCgThreads) {
@@ -107,8 +109,9 @@ __global__ void __launch_bounds__(kCgThreads, 4) coopg_solve_kernel(const __grid
   const double* __restrict__ v = a.W + (size_t)k * c.nnz_LU;
   auto vg = [v](int i) { return v[i]; };
   auto ys = [](int i) { return y[i]; };
+  const double* __restrict__ B = a.B + (size_t)a.mj.jac(k) * a.mj.b_stride;
   for (int r = 0; r < a.R; ++r) {
-    for (int i = tid; i < c.n; i += kCgThreads) y[i] = a.B[(size_t)r * a.ldb + a.perm[i]];
+    for (int i = tid; i < c.n; i += kCgThreads) y[i] = B[(size_t)r * a.ldb + a.perm[i]];
     __syncthreads();
     for (int step = 0; step < c.steps; ++step) {   // forward: y_i = fma(-l_ip, y_p, y_i), p ascending
       for (int j = c.ya_ptr[step] + tid; j < c.ya_ptr[step + 1]; j += kCgThreads) {

@@ -5,6 +5,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "psp_internal.h"
+
 namespace psp {
 
 // The CoopPlan of psp_plan.h with 32-bit fields (device arrays).
@@ -34,6 +36,7 @@ struct CoopGArgs {
   double tol_value = 0.0;
   double* W = nullptr;             // [K][nnz_LU] lane-major factor images (positions of V)
   int32_t* status = nullptr;
+  MultiJac mj;                     // (multi-Jacobian batches)
 };
 
 struct CoopGSolveArgs {
@@ -44,6 +47,7 @@ struct CoopGSolveArgs {
   int64_t ldb = 0;
   int32_t R = 0;
   double* X = nullptr;             // [K/32][R][n][32]
+  MultiJac mj;
 };
 
 size_t coopg_solve_smem(int n);

@@ -86,7 +86,9 @@ __global__ void __launch_bounds__(kDThreads, 1) dense_lu_kernel(const __grid_con
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* __restrict__ Mk = a.M + (size_t)k * N * N;
   const double e = a.eps[k];
-  const double tol = a.tol_dev ? *a.tol_dev : a.tol_value;
+  const int jac = a.mj.jac(k);
+  const double* __restrict__ Aj = a.A + (size_t)jac * a.mj.a_stride;
+  const double tol = a.tol_dev ? a.tol_dev[jac] : a.tol_value;
 
   // 1. perturb: M_k = P (A + e D) P^T (diagonal D: a_ii + (e d_i), off-diagonal a_ij;
   //    dense D: a_ij + (e D_ij) for every entry, a_ij = 0 outside the pattern)
@@ -107,7 +109,7 @@ __global__ void __launch_bounds__(kDThreads, 1) dense_lu_kernel(const __grid_con
     if (i < n) {
       for (int q = a.rp[i] + lane; q < a.rp[i + 1]; q += 32) {
         const int j = a.ci[q];
-        const double av = a.A[a.src[q]];
+        const double av = Aj[a.src[q]];
         double v;
         if (kDenseD) v = av + e * a.Dp[(size_t)i * n + j];
         else v = (j == i) ? av + e * a.dperm[i] : av;
@@ -230,10 +232,11 @@ __global__ void __launch_bounds__(kDThreads, 2) dense_solve_kernel(const __grid_
   const int k = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double* __restrict__ Mk = a.M + (size_t)k * N * N;
+  const double* __restrict__ Bk = a.B + (size_t)a.mj.jac(k) * a.mj.b_stride;
   for (int rc0 = 0; rc0 < R; rc0 += kDRC) {
     for (int idx = tid; idx < N * kDRC; idx += kDThreads) {
       const int i = idx / kDRC, r = idx - i * kDRC;
-      Y[idx] = (i < n && rc0 + r < R) ? a.B[(size_t)(rc0 + r) * a.ldb + a.perm[i]] : 0.0;
+      Y[idx] = (i < n && rc0 + r < R) ? Bk[(size_t)(rc0 + r) * a.ldb + a.perm[i]] : 0.0;
     }
     __syncthreads();
     // forward: y = L^{-1} P b (unit lower), y_i receiving its updates in ascending j

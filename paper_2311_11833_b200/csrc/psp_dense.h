@@ -6,6 +6,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "psp_internal.h"
+
 namespace psp {
 
 struct DenseArgs {
@@ -21,6 +23,7 @@ struct DenseArgs {
   double tol_value = 0.0;
   double* M = nullptr;                  // [K][N][N] row-major factors
   int32_t* status = nullptr;            // [K]
+  MultiJac mj;                          // (multi-Jacobian batches)
 };
 
 struct DenseSolveArgs {
@@ -30,6 +33,7 @@ struct DenseSolveArgs {
   const double* M = nullptr;            // [K][N][N] factors
   const double* B = nullptr;            // n x R column-major (ldb)
   double* X = nullptr;                  // [K/32][R][n][32], permuted rows
+  MultiJac mj;
 };
 
 int dense_padded_order(int n);

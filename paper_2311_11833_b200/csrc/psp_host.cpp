@@ -107,6 +107,7 @@ struct psp_ctx {
   bool coopg_ok = false;
   int64_t opt_coopg = 0;           // PSP_OPT_COOP_GLOBAL: 0 automatic, 1 on, 2 off
   bool coopg_factored = false;     // the last factorisation ran them (V_d is lane-major)
+  psp::MultiJac mj;                // multi-Jacobian layout of the last factorisation
   // program of the augmented matrix [A | b] (psp_factor_solve_batch); its own slots,
   // stream and factor launch configuration, the rest shared with `plan`
   DevicePlan plan_aug;
@@ -1033,7 +1034,7 @@ static bool use_spill(psp_ctx* h, bool aug) {
 
 // Dense path (psp_dense.cu): K padded N x N factors, one CTA per lane.
 static psp_status dense_factor(psp_handle h, const double* A_vals, double pivot_tol,
-                               int32_t* lane_status) {
+                               int32_t* lane_status, psp::MultiJac mj = psp::MultiJac{}) {
   if (h->growth) return fail(h, PSP_ERR_UNSUPPORTED, "PSP_OPT_GROWTH is a sparse-path pass");
   const int32_t N = h->dense_N;
   cudaSetDevice(h->device);
@@ -1051,10 +1052,12 @@ static psp_status dense_factor(psp_handle h, const double* A_vals, double pivot_
   }
   const double* tol_dev = nullptr;
   if (pivot_tol <= 0) {
-    CUDA_TRY(h, psp::launch_pivot_tol(h->plan, A_vals, (double*)h->tol_d.p, h->stream));
+    CUDA_TRY(h, psp::launch_pivot_tol(h->plan, A_vals, (double*)h->tol_d.p, h->stream,
+                                      mj.lanes_per > 0 ? h->K / mj.lanes_per : 1));
     tol_dev = (const double*)h->tol_d.p;
   }
   psp::DenseArgs a;
+  a.mj = mj;
   a.n = h->n;
   a.N = N;
   a.rp = h->drp_d;
@@ -1084,11 +1087,13 @@ static psp_status dense_factor(psp_handle h, const double* A_vals, double pivot_
   h->factored = true;
   h->dense_factored = true;
   h->coopg_factored = false;
+  h->mj = mj;
   h->solved = h->recovered = false;
   return PSP_OK;
 }
 
-static psp_status dense_solve(psp_handle h, int32_t R, const double* B, int64_t ldb) {
+static psp_status dense_solve(psp_handle h, int32_t R, const double* B, int64_t ldb,
+                              psp::MultiJac mj = psp::MultiJac{}) {
   psp_status s;
   if (h->phase_events) {
     if ((s = phase_mark(h, h->sev, h->ns))) return s;
@@ -1102,6 +1107,7 @@ static psp_status dense_solve(psp_handle h, int32_t R, const double* B, int64_t 
   a.M = (const double*)h->Md_d.p;
   a.B = B;
   a.X = (double*)h->X_d.p;
+  a.mj = mj;
   h->last_solve = PSP_KERNEL_DENSE;
   h->last_solve_fwd = 1;
   CUDA_TRY(h, psp::launch_dense_solve(a, h->K, h->stream));
@@ -1115,7 +1121,7 @@ static psp_status dense_solve(psp_handle h, int32_t R, const double* B, int64_t 
 
 // Global-memory level-scheduled factor (psp_coopg.cu): V_d holds lane-major images.
 static psp_status coopg_factor(psp_handle h, const double* A_vals, double pivot_tol,
-                               int32_t* lane_status) {
+                               int32_t* lane_status, psp::MultiJac mj = psp::MultiJac{}) {
   if (h->growth) return fail(h, PSP_ERR_UNSUPPORTED, "PSP_OPT_GROWTH reads the batch factor layout");
   cudaSetDevice(h->device);
   psp_status s;
@@ -1125,10 +1131,12 @@ static psp_status coopg_factor(psp_handle h, const double* A_vals, double pivot_
   a.eps = (const double*)h->eps_d.p;
   a.dperm = (const double*)h->dperm_d.p;
   if (pivot_tol <= 0) {
-    CUDA_TRY(h, psp::launch_pivot_tol(h->plan, A_vals, (double*)h->tol_d.p, h->stream));
+    CUDA_TRY(h, psp::launch_pivot_tol(h->plan, A_vals, (double*)h->tol_d.p, h->stream,
+                                      mj.lanes_per > 0 ? h->K / mj.lanes_per : 1));
     a.tol_dev = (const double*)h->tol_d.p;
   }
   a.tol_value = pivot_tol;
+  a.mj = mj;
   a.W = (double*)h->V_d.p;   // (K_pad x nnz_LU doubles: the same bytes as the batch layout)
   a.status = (int32_t*)h->status_d.p;
   if (h->phase_events) {
@@ -1147,11 +1155,13 @@ static psp_status coopg_factor(psp_handle h, const double* A_vals, double pivot_
   h->factored = true;
   h->dense_factored = false;
   h->coopg_factored = true;
+  h->mj = mj;
   h->solved = h->recovered = false;
   return PSP_OK;
 }
 
-static psp_status coopg_solve(psp_handle h, int32_t R, const double* B, int64_t ldb) {
+static psp_status coopg_solve(psp_handle h, int32_t R, const double* B, int64_t ldb,
+                              psp::MultiJac mj = psp::MultiJac{}) {
   psp_status s;
   if (h->phase_events) {
     if ((s = phase_mark(h, h->sev, h->ns))) return s;
@@ -1164,6 +1174,7 @@ static psp_status coopg_solve(psp_handle h, int32_t R, const double* B, int64_t 
   a.ldb = ldb;
   a.R = R;
   a.X = (double*)h->X_d.p;
+  a.mj = mj;
   h->last_solve = PSP_KERNEL_COOP_GLOBAL;
   h->last_solve_fwd = 1;
   CUDA_TRY(h, psp::launch_coopg_solve(a, h->K, h->stream));
@@ -1176,15 +1187,20 @@ static psp_status coopg_solve(psp_handle h, int32_t R, const double* B, int64_t 
 }
 
 static psp_status factor_impl(psp_handle h, const double* A_vals, double pivot_tol,
-                              int32_t* lane_status, bool aug, const double* b) {
+                              int32_t* lane_status, bool aug, const double* b,
+                              psp::MultiJac mj = psp::MultiJac{}) {
   if (!h) return PSP_ERR_ARG;
   if (!h->analysed || h->K == 0) return fail(h, PSP_ERR_STATE, "set_perturbations first");
   if (!A_vals) return fail(h, PSP_ERR_ARG, "A_vals required");
   if (!(pivot_tol == pivot_tol)) return fail(h, PSP_ERR_ARG, "pivot_tol is NaN");
-  if (h->opt_path == PSP_PATH_DENSE) return dense_factor(h, A_vals, pivot_tol, lane_status);
+  if (h->opt_path == PSP_PATH_DENSE) return dense_factor(h, A_vals, pivot_tol, lane_status, mj);
   if (h->dense_D)
     return fail(h, PSP_ERR_UNSUPPORTED, "a dense D needs the dense path (PSP_OPT_PATH = PSP_PATH_DENSE)");
-  if (use_coopg(h)) return coopg_factor(h, A_vals, pivot_tol, lane_status);
+  if (use_coopg(h)) return coopg_factor(h, A_vals, pivot_tol, lane_status, mj);
+  if (mj.lanes_per > 0 && !use_coop(h))
+    return fail(h, PSP_ERR_UNSUPPORTED,
+                "multi-Jacobian batches run the cooperative / global level-scheduled / dense kernels "
+                "(K <= 8 x SMs, or PSP_OPT_COOP = 1); factor larger batches per Jacobian");
   const bool spill = !use_coop(h) && use_spill(h, aug);
   const DevicePlan& P = spill ? (aug ? h->plan_spill_aug : h->plan_spill) : (aug ? h->plan_aug : h->plan);
   const psp::LaunchInfo& LI = spill ? (aug ? h->launch_spill_aug : h->launch_spill)
@@ -1193,7 +1209,8 @@ static psp_status factor_impl(psp_handle h, const double* A_vals, double pivot_t
   psp_status s;
   const double* tol_dev = nullptr;
   if (pivot_tol <= 0) {
-    CUDA_TRY(h, psp::launch_pivot_tol(P, A_vals, (double*)h->tol_d.p, h->stream));
+    CUDA_TRY(h, psp::launch_pivot_tol(P, A_vals, (double*)h->tol_d.p, h->stream,
+                                      mj.lanes_per > 0 ? h->K / mj.lanes_per : 1));
     tol_dev = (const double*)h->tol_d.p;
   }
   if (!LI.f_pend_smem) {
@@ -1240,7 +1257,7 @@ static psp_status factor_impl(psp_handle h, const double* A_vals, double pivot_t
     CUDA_TRY(h, psp::launch_coop_factor(h->plan, h->coop, A_vals, (const double*)h->eps_d.p,
                                         (const double*)h->dperm_d.p, tol_dev, pivot_tol,
                                         (double*)h->V_d.p, (int32_t*)h->status_d.p, h->K,
-                                        kBlock / h->launch.f_groups * h->launch.f_lanes, h->stream));
+                                        kBlock / h->launch.f_groups * h->launch.f_lanes, h->stream, mj));
   } else {
     h->last_factor = spill ? PSP_KERNEL_BATCH_SPILL : (LI.f_tmem ? PSP_KERNEL_BATCH_TMEM : PSP_KERNEL_BATCH);
     h->last_factor_aug = aug ? 1 : 0;
@@ -1264,6 +1281,7 @@ static psp_status factor_impl(psp_handle h, const double* A_vals, double pivot_t
   h->factored = true;
   h->dense_factored = false;
   h->coopg_factored = false;
+  h->mj = mj;
   h->solved = h->recovered = false;
   return PSP_OK;
 }
@@ -1354,6 +1372,57 @@ psp_status psp_solve_batch(psp_handle h, int32_t R, const double* B, int64_t ldb
   CUDA_TRY(h, psp::launch_solve(h->plan, solve_launch(h, R), (const double*)h->V_d.p, B, ldb, R,
                                 (double*)h->X_d.p, (double*)h->sscratch_d.p, h->K_pad, true,
                                 h->stream));
+  if (h->phase_events) {
+    if ((s = phase_mark(h, h->sev, h->ns))) return s;
+  }
+  h->R = R;
+  h->solved = true;
+  return PSP_OK;
+}
+
+psp_status psp_factor_batch_multi(psp_handle h, int32_t n_jac, const double* A_vals, double pivot_tol,
+                                  int32_t* lane_status) {
+  if (!h) return PSP_ERR_ARG;
+  if (!h->analysed || h->K == 0) return fail(h, PSP_ERR_STATE, "set_perturbations first");
+  if (n_jac < 1 || h->K % n_jac) return fail(h, PSP_ERR_ARG, "n_jac >= 1 must divide K = %d", h->K);
+  if (n_jac == 1) return psp_factor_batch(h, A_vals, pivot_tol, lane_status);
+  psp_status s;
+  if (h->tol_d.bytes < sizeof(double) * (size_t)n_jac) {
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    if ((s = ensure(h, h->tol_d, sizeof(double) * (size_t)n_jac))) return s;
+  }
+  psp::MultiJac mj;
+  mj.lanes_per = h->K / n_jac;
+  mj.a_stride = h->nnz_A;
+  return factor_impl(h, A_vals, pivot_tol, lane_status, false, nullptr, mj);
+}
+
+psp_status psp_solve_batch_multi(psp_handle h, int32_t R, const double* B, int64_t ldb, int64_t jac_stride) {
+  if (!h) return PSP_ERR_ARG;
+  if (!h->factored || h->mj.lanes_per == 0)
+    return fail(h, PSP_ERR_STATE, "psp_factor_batch_multi (n_jac > 1) first");
+  if (R < 1 || !B || ldb < h->n || jac_stride < (int64_t)(R - 1) * ldb + h->n)
+    return fail(h, PSP_ERR_ARG, "R >= 1, B, ldb >= n, jac_stride >= (R - 1) ldb + n required");
+  cudaSetDevice(h->device);
+  psp_status s;
+  size_t need = sizeof(double) * (size_t)h->K_pad * R * h->n;
+  if (h->X_d.bytes < need) {
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    if ((s = ensure(h, h->X_d, need))) return s;
+  }
+  psp::MultiJac mj = h->mj;
+  mj.b_stride = jac_stride;
+  if (h->dense_factored) return dense_solve(h, R, B, ldb, mj);
+  if (h->coopg_factored) return coopg_solve(h, R, B, ldb, mj);
+  if (h->last_factor != PSP_KERNEL_COOP)
+    return fail(h, PSP_ERR_UNSUPPORTED, "multi-Jacobian solves follow a multi-Jacobian factorisation");
+  if (h->phase_events) {
+    if ((s = phase_mark(h, h->sev, h->ns))) return s;
+  }
+  h->last_solve = PSP_KERNEL_COOP;
+  h->last_solve_fwd = 1;
+  CUDA_TRY(h, psp::launch_coop_solve(h->plan, h->coop, (const double*)h->V_d.p, B, ldb, R, (double*)h->X_d.p,
+                                     h->K, kBlock / h->launch.f_groups * h->launch.f_lanes, h->stream, mj));
   if (h->phase_events) {
     if ((s = phase_mark(h, h->sev, h->ns))) return s;
   }

@@ -56,6 +56,15 @@ struct DevicePlan {
   const int32_t* acsc_q = nullptr;     // [nnz_A]
 };
 
+// Multi-Jacobian batches (many Jacobians of one pattern in one launch):
+// lane k uses Jacobian jac(k) = k / lanes_per (0 = a single Jacobian): its values at
+// A + jac * a_stride, its right-hand sides at B + jac * b_stride, its tolerance tol[jac].
+struct MultiJac {
+  int32_t lanes_per = 0;
+  int64_t a_stride = 0, b_stride = 0;
+  __host__ __device__ int jac(int k) const { return lanes_per > 0 ? k / lanes_per : 0; }
+};
+
 // Device copy of the level-scheduled plan of the cooperative small-batch kernels
 // (psp_plan.h CoopPlan): one CTA per system, its factor image in shared memory.
 struct CoopDev {
@@ -76,10 +85,10 @@ struct CoopDev {
 cudaError_t launch_coop_factor(const DevicePlan& p, const CoopDev& c, const double* A,
                                const double* eps, const double* dperm, const double* tol_dev,
                                double tol_value, double* V, int32_t* status, int32_t K, int32_t LS,
-                               cudaStream_t stream);
+                               cudaStream_t stream, MultiJac mj = MultiJac{});
 cudaError_t launch_coop_solve(const DevicePlan& p, const CoopDev& c, const double* V, const double* B,
                               int64_t ldb, int32_t R, double* X, int32_t K, int32_t LS,
-                              cudaStream_t stream);
+                              cudaStream_t stream, MultiJac mj = MultiJac{});
 size_t coop_smem_bytes(const DevicePlan& p, const CoopDev& c, bool solve);
 cudaError_t configure_coop(const DevicePlan& p, const CoopDev& c);
 
@@ -130,7 +139,7 @@ cudaError_t configure_kernels(const DevicePlan& p, LaunchInfo& li, int force_gro
 cudaError_t launch_patch_program(const DevicePlan& p, int32_t* stream_out, const double* A_vals,
                                  const double* dperm, const double* b, cudaStream_t stream);
 cudaError_t launch_pivot_tol(const DevicePlan& p, const double* A_vals, double* tol_out,
-                             cudaStream_t stream);
+                             cudaStream_t stream, int32_t n_jac = 1);
 cudaError_t launch_factor(const DevicePlan& p, const LaunchInfo& li, const int32_t* prog,
                           const double* eps, const double* tol_dev, double tol_value, double* V,
                           double* gscratch, double* gscr, int32_t* status, int32_t K_pad,

@@ -29,7 +29,7 @@ EXPORTS = ["psp_create", "psp_destroy", "psp_set_stream", "psp_status_string",
            "psp_rescale_failed_rows", "psp_get_perturbations", "psp_get_last_kernels",
            "psp_get_unique_id", "psp_comm_init", "psp_set_perturbations_shard", "psp_shard_weights",
            "psp_set_weights_dense", "psp_recover_reduce", "psp_get_dense_factor",
-           "psp_set_perturbation_matrix"]
+           "psp_set_perturbation_matrix", "psp_factor_batch_multi", "psp_solve_batch_multi"]
 KERNEL = {0: "none", 1: "coop", 2: "batch", 3: "batch_tmem", 4: "batch_spill", 5: "dense", 6: "coop_global"}
 PATH = {"sparse": 0, "dense": 1}
 OPT = {"factor_groups": 1, "factor_warps": 2, "factor_lanes": 3, "factor_slab_warps": 4,
@@ -109,6 +109,8 @@ def lib():
             "psp_recover_reduce": [P, P, I32],
             "psp_get_dense_factor": [P, I32, P],
             "psp_set_perturbation_matrix": [P, P],
+            "psp_factor_batch_multi": [P, I32, P, D, P],
+            "psp_solve_batch_multi": [P, I32, P, I64, I64],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -186,6 +188,26 @@ class Solver:
         if Dm.shape != (self.n, self.n):
             raise ValueError("D must be n x n")
         self._check(lib().psp_set_perturbation_matrix(self.h, _np_ptr(Dm)))
+
+    def psp_factor_batch_multi(self, A_vals, pivot_tol=0.0, lane_status=None):
+        """A_vals: device [n_jac, nnz_A]; lane k uses Jacobian k // (K // n_jac)."""
+        if A_vals.dim() != 2 or A_vals.shape[1] != self.nnz_A:
+            raise ValueError("A_vals must be [n_jac, nnz_A]")
+        self._check_dev(A_vals, self.torch.float64, tuple(A_vals.shape))
+        ls = None
+        if lane_status is not None:
+            self._check_dev(lane_status, self.torch.int32, (self.K,))
+            ls = _t_ptr(lane_status)
+        self._check(lib().psp_factor_batch_multi(self.h, int(A_vals.shape[0]), _t_ptr(A_vals), float(pivot_tol), ls))
+
+    def psp_solve_batch_multi(self, B):
+        """B: device [n_jac, R, n] (each Jacobian's right-hand sides, original ordering)."""
+        if B.dim() != 3 or B.shape[2] != self.n:
+            raise ValueError("B must be [n_jac, R, n]")
+        self._check_dev(B, self.torch.float64, tuple(B.shape))
+        R = int(B.shape[1])
+        self._check(lib().psp_solve_batch_multi(self.h, R, _t_ptr(B), self.n, R * self.n))
+        self.R = R
 
     def psp_get_dense_factor(self, k):
         """Lane k's dense factor (host numpy n x n, permuted order; L strict lower, U upper)."""
