@@ -67,6 +67,8 @@ def lib():
         L.oracle_combine.restype = None
         L.oracle_num_threads.restype = I
         L.oracle_set_num_threads.argtypes = [I]
+        L.oracle_residual_fma.argtypes = [I, P, P, P, P, P, P]
+        L.oracle_residual_fma.restype = None
         _lib = L
     return _lib
 
@@ -337,6 +339,51 @@ def predicted_error(sysm, mags, B=None, Dm=None):
             v = (s * s) * M(M(u))
         out[r] = (-1.0) ** len(mags) * v
     return out
+
+
+def residual_fma(sysm, x, b):
+    """r = b - A x row by row, one fma per CSR entry in order (oracle.c) -> [n]."""
+    r = np.empty(sysm.n)
+    lib().oracle_residual_fma(sysm.n, _p(_c(sysm.row_ptr, np.int32)), _p(_c(sysm.col_idx, np.int32)),
+                              _p(_c(sysm.vals, np.float64)), _p(_c(x, np.float64)), _p(_c(b, np.float64)),
+                              _p(r))
+    return r
+
+
+def refine(sysm, perm, eps, tol, iters, b=None):
+    """Iterative-refinement baseline: static pivoting by a
+    perturbation plus fixed-precision iterative refinement against the UNPERTURBED A, per
+    lane k, with F_k = P (A + eps_k D) P^T factored without pivoting (lu_nopivot):
+        x^0 = F_k^{-1} b;   x^i = x^{i-1} + F_k^{-1} (b - A x^{i-1})   (i = 1..iters),
+    the residual by residual_fma, the correction by lu_solve, the update one rounded add.
+    In exact arithmetic e^i = x* - x^i = (I - F^{-1} A) e^{i-1} = eps_k M_k e^{i-1} and
+    e^0 = eps_k M_k x*, so e^i = (eps_k M_k)^{i+1} x* with M_k = (A + eps_k D)^{-1} D.  Returns X [iters + 1, K, n] (original ordering; NaN
+    for a failed lane) and status [K]."""
+    b = sysm.b[:, 0] if b is None else np.asarray(b, dtype=np.float64)
+    A = _dense(sysm)
+    d = np.asarray(sysm.d, dtype=np.float64)
+    perm = np.asarray(perm, dtype=np.int64)
+    eps = np.asarray(eps, dtype=np.float64)
+    X = np.full((iters + 1, len(eps), sysm.n), np.nan)
+    st = np.zeros(len(eps), dtype=np.int32)
+    for k, e in enumerate(eps):
+        Ak = A.copy()
+        Ak[np.diag_indices(sysm.n)] = np.diag(A) + e * d          # a_ii + (eps d_i)
+        LU, st[k] = lu_nopivot(Ak[np.ix_(perm, perm)], tol)
+        if st[k]:
+            continue
+
+        def solve(rhs):
+            out = np.empty(sysm.n)
+            out[perm] = lu_solve(LU, rhs[perm])
+            return out
+
+        x = solve(b)
+        X[0, k] = x
+        for i in range(1, iters + 1):
+            x = x + solve(residual_fma(sysm, x, b))
+            X[i, k] = x
+    return X, st
 
 
 def residual(sysm, X, B=None):

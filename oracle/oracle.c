@@ -269,3 +269,17 @@ void oracle_combine(int K, int R, int n, int W, const double* weights, const dou
         out[((size_t)w * R + r) * n + i] = acc;
       }
 }
+
+/* ------------------------------------------------------------------------- */
+/* Iterative-refinement baseline ("compared with
+ * existing iterative refinement-based approaches"): the residual of one iterate,
+ * r = b - A x, row by row over the CSR entries in order, one fma per term:
+ * r_i = b_i; for q: r_i = fma(-a_iq, x_{col q}, r_i).                            */
+void oracle_residual_fma(int n, const int32_t* rp, const int32_t* ci, const double* v,
+                         const double* x, const double* b, double* r) {
+  for (int i = 0; i < n; ++i) {
+    double acc = b[i];
+    for (int q = rp[i]; q < rp[i + 1]; ++q) acc = fma(-v[q], x[ci[q]], acc);
+    r[i] = acc;
+  }
+}
