@@ -272,6 +272,20 @@ psp_status psp_factor_batch_multi(psp_handle h, int32_t n_jac, const double* A_v
  * ALLOC, CUDA. */
 psp_status psp_solve_batch_multi(psp_handle h, int32_t R, const double* B, int64_t ldb, int64_t jac_stride);
 
+/* Iterative-refinement baseline (the comparison P:L336 asks for):
+ * static pivoting by one perturbation per lane plus fixed-precision iterative refinement
+ * against the UNPERTURBED A, every lane k with its own factor F_k = A + eps_k D from the
+ * last factorisation:  x^0 = F_k^{-1} b;  x^i = x^{i-1} + F_k^{-1} (b - A x^{i-1}), i = 1..iters
+ * (residual one fma per CSR entry in order, the correction by the factor's substitutions,
+ * the update one rounded add -- bitwise the oracle's refine).  Converges to x* when
+ * |eps_k| rho((A + eps_k D)^{-1} D) < 1: x* - x^i = (eps_k M_k)^{i+1} x*.  A_vals: the
+ * (device) values the factorisation used; b: device n values, ORIGINAL ordering; x_out:
+ * device K x n (lane-major, ORIGINAL ordering) receives x^iters.  Needs per-lane
+ * right-hand sides: the cooperative, global level-scheduled or dense kernels; else
+ * PSP_ERR_UNSUPPORTED.  Overwrites the handle's solutions (psp_get_solutions: solve again).
+ * Errors: ARG, STATE, UNSUPPORTED, ALLOC, CUDA. */
+psp_status psp_refine(psp_handle h, const double* A_vals, const double* b, int32_t iters, double* x_out);
+
 /* Spectral radius rho(A^-1 D) by power iteration (Eq. (4)'s rho; the convergence
  * premise eps_c = m eps < 1 / rho of Theorem 1),
  * reusing the handle's factorisation: A^-1 r is applied as the recovered solution w of

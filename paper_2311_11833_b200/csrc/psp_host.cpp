@@ -140,6 +140,7 @@ struct psp_ctx {
   const int32_t* rowptr_d = nullptr;   // plan buffers: the analysed CSR pattern (psp_residual)
   const int32_t* colidx_d = nullptr;
   DevBuf res_d;                        // psp_residual output
+  DevBuf ref_r_d;                      // psp_refine: per-lane residuals [K][n]
   std::vector<cudaEvent_t> fev, sev;
   size_t nf = 0, ns = 0;
 
@@ -1428,6 +1429,51 @@ psp_status psp_solve_batch_multi(psp_handle h, int32_t R, const double* B, int64
   }
   h->R = R;
   h->solved = true;
+  return PSP_OK;
+}
+
+psp_status psp_refine(psp_handle h, const double* A_vals, const double* b, int32_t iters, double* x_out) {
+  if (!h) return PSP_ERR_ARG;
+  if (!h->factored) return fail(h, PSP_ERR_STATE, "factor_batch first");
+  if (!A_vals || !b || !x_out || iters < 0) return fail(h, PSP_ERR_ARG, "A_vals, b, x_out, iters >= 0 required");
+  if (h->mj.lanes_per > 0) return fail(h, PSP_ERR_UNSUPPORTED, "psp_refine follows a single-Jacobian factorisation");
+  const bool coop = !h->dense_factored && !h->coopg_factored && h->last_factor == PSP_KERNEL_COOP;
+  if (!h->dense_factored && !h->coopg_factored && !coop)
+    return fail(h, PSP_ERR_UNSUPPORTED,
+                "psp_refine needs per-lane right-hand sides: the cooperative, global level-scheduled or "
+                "dense kernels (K <= 8 x SMs, PSP_OPT_COOP / PSP_OPT_COOP_GLOBAL, or PSP_OPT_PATH)");
+  cudaSetDevice(h->device);
+  psp_status s;
+  // x^0 = F_k^{-1} b
+  if ((s = psp_solve_batch(h, 1, b, h->n))) return s;
+  CUDA_TRY(h, psp::launch_gather_solutions(h->plan, h->K, 1, (const double*)h->X_d.p, x_out, h->stream));
+  if (iters == 0) return PSP_OK;
+  const size_t need = sizeof(double) * (size_t)h->K * h->n;
+  if (h->ref_r_d.bytes < need) {
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    if ((s = ensure(h, h->ref_r_d, need))) return s;
+  }
+  psp::MultiJac mj;          // each lane its own right-hand side r_k
+  mj.lanes_per = 1;
+  mj.b_stride = h->n;
+  double* r = (double*)h->ref_r_d.p;
+  for (int32_t it = 0; it < iters; ++it) {
+    CUDA_TRY(h, psp::launch_refine_step(h->plan, h->K, h->rowptr_d, h->colidx_d, A_vals, b, x_out, r, h->stream));
+    if (h->dense_factored) {
+      if ((s = dense_solve(h, 1, r, h->n, mj))) return s;
+    } else if (h->coopg_factored) {
+      if ((s = coopg_solve(h, 1, r, h->n, mj))) return s;
+    } else {
+      h->last_solve = PSP_KERNEL_COOP;
+      h->last_solve_fwd = 1;
+      CUDA_TRY(h, psp::launch_coop_solve(h->plan, h->coop, (const double*)h->V_d.p, r, h->n, 1,
+                                         (double*)h->X_d.p, h->K,
+                                         kBlock / h->launch.f_groups * h->launch.f_lanes, h->stream, mj));
+    }
+    CUDA_TRY(h, psp::launch_refine_update(h->plan, h->K, (const double*)h->X_d.p, x_out, h->stream));
+  }
+  h->solved = false;   // (X holds the last correction, not solutions)
+  h->recovered = false;
   return PSP_OK;
 }
 

@@ -165,6 +165,11 @@ cudaError_t launch_recover_seg(const DevicePlan& p, int32_t W, int32_t R, const 
                                const int32_t* w_lane, const double* w_val, const double* X,
                                const int32_t* status, double* x_out, int32_t* flag,
                                cudaStream_t stream);
+// Iterative-refinement baseline: r = b - A x per lane ([K][n], original ordering), and
+// x += (the correction in X, batch layout, R = 1).
+cudaError_t launch_refine_step(const DevicePlan& p, int32_t K, const int32_t* row_ptr, const int32_t* col_idx,
+                               const double* A, const double* b, const double* x, double* r, cudaStream_t stream);
+cudaError_t launch_refine_update(const DevicePlan& p, int32_t K, const double* X, double* x, cudaStream_t stream);
 cudaError_t launch_gather_solutions(const DevicePlan& p, int32_t K, int32_t R, const double* X,
                                     double* out, cudaStream_t stream);
 

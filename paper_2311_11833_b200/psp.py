@@ -29,7 +29,8 @@ EXPORTS = ["psp_create", "psp_destroy", "psp_set_stream", "psp_status_string",
            "psp_rescale_failed_rows", "psp_get_perturbations", "psp_get_last_kernels",
            "psp_get_unique_id", "psp_comm_init", "psp_set_perturbations_shard", "psp_shard_weights",
            "psp_set_weights_dense", "psp_recover_reduce", "psp_get_dense_factor",
-           "psp_set_perturbation_matrix", "psp_factor_batch_multi", "psp_solve_batch_multi"]
+           "psp_set_perturbation_matrix", "psp_factor_batch_multi", "psp_solve_batch_multi",
+           "psp_refine"]
 KERNEL = {0: "none", 1: "coop", 2: "batch", 3: "batch_tmem", 4: "batch_spill", 5: "dense", 6: "coop_global"}
 PATH = {"sparse": 0, "dense": 1}
 OPT = {"factor_groups": 1, "factor_warps": 2, "factor_lanes": 3, "factor_slab_warps": 4,
@@ -111,6 +112,7 @@ def lib():
             "psp_set_perturbation_matrix": [P, P],
             "psp_factor_batch_multi": [P, I32, P, D, P],
             "psp_solve_batch_multi": [P, I32, P, I64, I64],
+            "psp_refine": [P, P, P, I32, P],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -208,6 +210,17 @@ class Solver:
         R = int(B.shape[1])
         self._check(lib().psp_solve_batch_multi(self.h, R, _t_ptr(B), self.n, R * self.n))
         self.R = R
+
+    def psp_refine(self, A_vals, b, iters, out=None):
+        """Iterative-refinement baseline (include/psp.h): per lane, x^iters of the refinement
+        with the lane's factor against the unperturbed A -> device [K, n] (original order)."""
+        self._check_dev(A_vals, self.torch.float64, (self.nnz_A,))
+        self._check_dev(b, self.torch.float64, (self.n,))
+        out = out if out is not None else self.torch.empty((self.K, self.n), dtype=self.torch.float64,
+                                                           device=f"cuda:{self.device}")
+        self._check_dev(out, self.torch.float64, (self.K, self.n))
+        self._check(lib().psp_refine(self.h, _t_ptr(A_vals), _t_ptr(b), int(iters), _t_ptr(out)))
+        return out
 
     def psp_get_dense_factor(self, k):
         """Lane k's dense factor (host numpy n x n, permuted order; L strict lower, U upper)."""
