@@ -57,7 +57,9 @@ enum {
   PSP_ERR_CUDA = 6,              /* CUDA runtime error; detail string has the code   */
   PSP_ERR_ALLOC = 7,             /* device or host allocation failed                 */
   PSP_ERR_UNSUPPORTED = 8,       /* feature not available in this build / handle     */
-  PSP_ERR_NCCL = 9               /* NCCL error; detail string has NCCL's message     */
+  PSP_ERR_NCCL = 9,              /* NCCL error; detail string has NCCL's message     */
+  PSP_ERR_STRUCT_SINGULAR = 10   /* PSP_OPT_TRANSVERSAL: no perfect matching (the pattern
+                                    is structurally singular)                        */
 };
 
 /* Elimination orders for psp_symbolic_analyse (R13). */
@@ -158,6 +160,17 @@ psp_status psp_destroy(psp_handle h);
  *                         factor image lane-major in the handle's factor storage, the same
  *                         etree-level schedule: bitwise the batch kernels); 1: always (when
  *                         built: set before psp_symbolic_analyse); 2: never.  Bitwise-neutral.
+ *  PSP_OPT_TRANSVERSAL    0 (default); 1: the structural pre-pass of P:L304 ("the
+ *                         Hopcroft-Karp algorithm (which permutes a matrix by moving
+ *                         non-zeros onto the diagonal)"): the analysis computes a maximum
+ *                         matching q (columns -> rows, Hopcroft-Karp in a fixed order,
+ *                         DESIGN.md R20; psp_get_transversal) and analyses and factors
+ *                         A_hat = A[q, :] (zero-free diagonal) instead of A: every later call
+ *                         takes A's values and b in the caller's ordering and gathers them
+ *                         (A_hat x = b[q] has the same solution x); the perturbation
+ *                         eps_k d_j goes on A_hat's diagonal entry (j, j).  The analysis
+ *                         fails with PSP_ERR_STRUCT_SINGULAR when no perfect matching
+ *                         exists.  Not with a dense D or psp_estimate_rho (UNSUPPORTED).
  *  PSP_OPT_PATH           PSP_PATH_SPARSE (default) or PSP_PATH_DENSE: which kernels the
  *                         next factorisations run (may change at any time; the
  *                         solve follows the last factorisation).  DENSE is the paper's own
@@ -177,7 +190,8 @@ enum { PSP_PATH_SPARSE = 0, PSP_PATH_DENSE = 1 };
 enum { PSP_OPT_FACTOR_GROUPS = 1, PSP_OPT_FACTOR_WARPS = 2, PSP_OPT_FACTOR_LANES = 3,
        PSP_OPT_FACTOR_SLAB_WARPS = 4, PSP_OPT_FACTOR_PAIRS = 5, PSP_OPT_FACTOR_TMEM = 6,
        PSP_OPT_SOLVE_TMEM = 7, PSP_OPT_PHASE_EVENTS = 8, PSP_OPT_GROWTH = 9,
-       PSP_OPT_COOP = 10, PSP_OPT_FACTOR_SPILL = 11, PSP_OPT_PATH = 12, PSP_OPT_COOP_GLOBAL = 13 };
+       PSP_OPT_COOP = 10, PSP_OPT_FACTOR_SPILL = 11, PSP_OPT_PATH = 12, PSP_OPT_COOP_GLOBAL = 13,
+       PSP_OPT_TRANSVERSAL = 14 };
 psp_status psp_set_option(psp_handle h, int32_t option, int64_t value);
 
 /* Rebind the handle to another stream of the same device.  Synchronises the old stream
@@ -201,6 +215,10 @@ const char* psp_last_error_detail(psp_handle h);
 psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_h,
                                 const int32_t* col_idx_h, int32_t ordering,
                                 const int32_t* user_perm_h, int32_t first_node);
+
+/* PSP_OPT_TRANSVERSAL: q_h[n] receives the matching of the last analysis (row q[j] of A is
+ * row j of the analysed A_hat).  Errors: ARG, STATE (no transversal analysed). */
+psp_status psp_get_transversal(psp_handle h, int32_t* q_h);
 
 /* Statistics of the analysis; perm_h (may be NULL) receives perm[new] = old. */
 psp_status psp_get_symbolic_info(psp_handle h, psp_symbolic_info* info_h, int32_t* perm_h);

@@ -108,6 +108,14 @@ struct psp_ctx {
   int64_t opt_coopg = 0;           // PSP_OPT_COOP_GLOBAL: 0 automatic, 1 on, 2 off
   bool coopg_factored = false;     // the last factorisation ran them (V_d is lane-major)
   psp::MultiJac mj;                // multi-Jacobian layout of the last factorisation
+  // structural transversal (PSP_OPT_TRANSVERSAL): the analysed matrix is the
+  // row-permuted A_hat = A[q, :]; entry points gather A's values and b's rows into it
+  int64_t opt_transversal = 0;
+  bool transversal = false;
+  std::vector<int32_t> tq;             // q[j] = row of A placed at row j
+  const int32_t* tq_d = nullptr;       // plan buffers: q, and A_hat CSR index -> A CSR index
+  const int32_t* tamap_d = nullptr;
+  DevBuf tA_d, tB_d, tb2_d;            // gathered A_hat values, B_hat, refine's b_hat
   // program of the augmented matrix [A | b] (psp_factor_solve_batch); its own slots,
   // stream and factor launch configuration, the rest shared with `plan`
   DevicePlan plan_aug;
@@ -258,6 +266,9 @@ static void release_plan(psp_ctx* h) {
   h->isdiag_d = nullptr;
   h->rowptr_d = h->colidx_d = nullptr;
   h->drp_d = h->dci_d = h->dsrc_d = nullptr;
+  h->tq_d = h->tamap_d = nullptr;
+  h->transversal = false;
+  h->tq.clear();
   h->dense_N = 0;
   h->dense_configured = false;
   h->Dp_d.release();
@@ -302,6 +313,7 @@ const char* psp_status_string(psp_status s) {
     case PSP_ERR_ALLOC: return "PSP_ERR_ALLOC";
     case PSP_ERR_UNSUPPORTED: return "PSP_ERR_UNSUPPORTED";
     case PSP_ERR_NCCL: return "PSP_ERR_NCCL";
+    case PSP_ERR_STRUCT_SINGULAR: return "PSP_ERR_STRUCT_SINGULAR";
     default: return "PSP_ERR_UNKNOWN";
   }
 }
@@ -418,6 +430,10 @@ psp_status psp_set_option(psp_handle h, int32_t option, int64_t value) {
       if (value != 0 && value != 1 && value != 2)
         return fail(h, PSP_ERR_ARG, "PSP_OPT_FACTOR_SLAB_WARPS must be 0, 1 or 2");
       h->opt_slab_warps = value;
+      return PSP_OK;
+    case PSP_OPT_TRANSVERSAL:
+      if (value != 0 && value != 1) return fail(h, PSP_ERR_ARG, "PSP_OPT_TRANSVERSAL must be 0 or 1");
+      h->opt_transversal = value;
       return PSP_OK;
     case PSP_OPT_PATH:
       if (value != PSP_PATH_SPARSE && value != PSP_PATH_DENSE)
@@ -539,6 +555,28 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
   release_plan(h);
   reset_numeric(h);
   h->analysed = false;
+
+  // structural transversal: analyse A_hat = A[q, :] (zero-free diagonal) instead of A
+  std::vector<int32_t> t_rp, t_ci, t_amap, t_q;
+  if (h->opt_transversal) {
+    t_q = psp::transversal_hk(n, row_ptr_h, col_idx_h);
+    int32_t matched = 0;
+    for (int32_t j = 0; j < n; ++j) matched += t_q[j] >= 0;
+    if (matched < n)
+      return fail(h, PSP_ERR_STRUCT_SINGULAR, "structurally singular: a maximum matching covers %d of %d columns",
+                  matched, n);
+    t_rp.assign(n + 1, 0);
+    for (int32_t j = 0; j < n; ++j) {
+      const int32_t r = t_q[j];
+      for (int32_t q = row_ptr_h[r]; q < row_ptr_h[r + 1]; ++q) {
+        t_ci.push_back(col_idx_h[q]);
+        t_amap.push_back(q);
+      }
+      t_rp[j + 1] = (int32_t)t_ci.size();
+    }
+    row_ptr_h = t_rp.data();
+    col_idx_h = t_ci.data();
+  }
 
   const int32_t nnzA = row_ptr_h[n];
   // symmetric adjacency of A + A^T (no self loops), original numbering
@@ -886,6 +924,14 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
     if ((s = upload(h, dsrc, &h->dsrc_d))) return s;
     h->dense_N = psp::dense_padded_order(n);
   }
+  if (h->opt_transversal) {
+    if (!host_only) {
+      if ((s = upload(h, t_q, &h->tq_d))) return s;
+      if ((s = upload(h, t_amap, &h->tamap_d))) return s;
+    }
+    h->tq = t_q;
+    h->transversal = true;
+  }
   h->plan = P;
   h->perm = perm;
   h->n = n;
@@ -1009,6 +1055,38 @@ static bool use_coopg(psp_ctx* h) {
   return h->opt_coopg == 1 || h->K <= 8 * h->n_sm;
 }
 
+// Structural transversal: the caller's A values / right-hand sides -> the analysed A_hat =
+// A[q, :] (gathered on the handle's stream into library buffers; no-ops without it).
+static psp_status tv_A(psp_ctx* h, const double*& A, int32_t n_jac) {
+  if (!h->transversal || !A) return PSP_OK;
+  psp_status s;
+  const size_t need = sizeof(double) * (size_t)n_jac * h->nnz_A;
+  if (h->tA_d.bytes < need) {
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    if ((s = ensure(h, h->tA_d, need))) return s;
+  }
+  CUDA_TRY(h, psp::launch_gather_a(h->tamap_d, h->nnz_A, n_jac, A, (double*)h->tA_d.p, h->stream));
+  A = (const double*)h->tA_d.p;
+  return PSP_OK;
+}
+static psp_status tv_B(psp_ctx* h, const double*& B, int32_t R, int64_t& ldb, int32_t n_jac = 1,
+                       int64_t* jac_stride = nullptr, DevBuf* buf = nullptr) {
+  if (!h->transversal || !B) return PSP_OK;
+  DevBuf& b = buf ? *buf : h->tB_d;
+  psp_status s;
+  const size_t need = sizeof(double) * (size_t)n_jac * R * h->n;
+  if (b.bytes < need) {
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    if ((s = ensure(h, b, need))) return s;
+  }
+  CUDA_TRY(h, psp::launch_gather_b(h->tq_d, h->n, R, n_jac, B, ldb, jac_stride ? *jac_stride : 0, (double*)b.p,
+                                   h->stream));
+  B = (const double*)b.p;
+  ldb = h->n;
+  if (jac_stride) *jac_stride = (int64_t)R * h->n;
+  return PSP_OK;
+}
+
 // Record the next event of a phase pool on the handle's stream (growing the pool).
 static psp_status phase_mark(psp_ctx* h, std::vector<cudaEvent_t>& pool, size_t& used) {
   if (used == pool.size()) {
@@ -1032,6 +1110,8 @@ static bool use_spill(psp_ctx* h, bool aug) {
   const int64_t round = (int64_t)h->n_sm * L.f_warps * std::max(1, L.f_ctas_per_sm);
   return (int64_t)(h->K_pad / kBlock) > round;
 }
+
+static psp_status solve_impl(psp_handle h, int32_t R, const double* B, int64_t ldb);
 
 // Dense path (psp_dense.cu): K padded N x N factors, one CTA per lane.
 static psp_status dense_factor(psp_handle h, const double* A_vals, double pivot_tol,
@@ -1289,6 +1369,9 @@ static psp_status factor_impl(psp_handle h, const double* A_vals, double pivot_t
 
 psp_status psp_factor_batch(psp_handle h, const double* A_vals, double pivot_tol,
                             int32_t* lane_status) {
+  if (!h) return PSP_ERR_ARG;
+  psp_status s;
+  if (h->analysed && h->K > 0 && (s = tv_A(h, A_vals, 1))) return s;
   return factor_impl(h, A_vals, pivot_tol, lane_status, false, nullptr);
 }
 
@@ -1310,14 +1393,19 @@ psp_status psp_factor_solve_batch(psp_handle h, const double* A_vals, const doub
   if (!h) return PSP_ERR_ARG;
   if (!b) return fail(h, PSP_ERR_ARG, "b required");
   psp_status s;
+  if (h->analysed && h->K > 0) {
+    int64_t ldb = h->n;
+    if ((s = tv_A(h, A_vals, 1))) return s;
+    if ((s = tv_B(h, b, 1, ldb))) return s;
+  }
   if (h->analysed && (h->opt_path == PSP_PATH_DENSE || use_coopg(h))) {
     if ((s = factor_impl(h, A_vals, pivot_tol, lane_status, false, nullptr))) return s;
-    return psp_solve_batch(h, 1, b, h->n);
+    return solve_impl(h, 1, b, h->n);
   }
   const bool fuse = h->analysed && !use_coop(h) && (use_spill(h, true) || h->aug_fast);
   if (h->analysed && !fuse) {   // the two calls (bitwise the same)
     if ((s = factor_impl(h, A_vals, pivot_tol, lane_status, false, nullptr))) return s;
-    return psp_solve_batch(h, 1, b, h->n);
+    return solve_impl(h, 1, b, h->n);
   }
   s = factor_impl(h, A_vals, pivot_tol, lane_status, true, b);
   if (s) return s;
@@ -1342,6 +1430,13 @@ psp_status psp_solve_batch(psp_handle h, int32_t R, const double* B, int64_t ldb
   if (!h) return PSP_ERR_ARG;
   if (!h->factored) return fail(h, PSP_ERR_STATE, "factor_batch first");
   if (R < 1 || !B || ldb < h->n) return fail(h, PSP_ERR_ARG, "R >= 1, B, ldb >= n required");
+  cudaSetDevice(h->device);
+  psp_status s;
+  if ((s = tv_B(h, B, R, ldb))) return s;
+  return solve_impl(h, R, B, ldb);
+}
+
+static psp_status solve_impl(psp_handle h, int32_t R, const double* B, int64_t ldb) {
   cudaSetDevice(h->device);
   psp_status s;
   size_t need = sizeof(double) * (size_t)h->K_pad * R * h->n;
@@ -1388,6 +1483,7 @@ psp_status psp_factor_batch_multi(psp_handle h, int32_t n_jac, const double* A_v
   if (n_jac < 1 || h->K % n_jac) return fail(h, PSP_ERR_ARG, "n_jac >= 1 must divide K = %d", h->K);
   if (n_jac == 1) return psp_factor_batch(h, A_vals, pivot_tol, lane_status);
   psp_status s;
+  if ((s = tv_A(h, A_vals, n_jac))) return s;
   if (h->tol_d.bytes < sizeof(double) * (size_t)n_jac) {
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     if ((s = ensure(h, h->tol_d, sizeof(double) * (size_t)n_jac))) return s;
@@ -1411,6 +1507,7 @@ psp_status psp_solve_batch_multi(psp_handle h, int32_t R, const double* B, int64
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     if ((s = ensure(h, h->X_d, need))) return s;
   }
+  if ((s = tv_B(h, B, R, ldb, h->K / h->mj.lanes_per, &jac_stride))) return s;
   psp::MultiJac mj = h->mj;
   mj.b_stride = jac_stride;
   if (h->dense_factored) return dense_solve(h, R, B, ldb, mj);
@@ -1444,8 +1541,11 @@ psp_status psp_refine(psp_handle h, const double* A_vals, const double* b, int32
                 "dense kernels (K <= 8 x SMs, PSP_OPT_COOP / PSP_OPT_COOP_GLOBAL, or PSP_OPT_PATH)");
   cudaSetDevice(h->device);
   psp_status s;
+  int64_t ldb1 = h->n;
+  if ((s = tv_A(h, A_vals, 1))) return s;
+  if ((s = tv_B(h, b, 1, ldb1, 1, nullptr, &h->tb2_d))) return s;
   // x^0 = F_k^{-1} b
-  if ((s = psp_solve_batch(h, 1, b, h->n))) return s;
+  if ((s = solve_impl(h, 1, b, h->n))) return s;
   CUDA_TRY(h, psp::launch_gather_solutions(h->plan, h->K, 1, (const double*)h->X_d.p, x_out, h->stream));
   if (iters == 0) return PSP_OK;
   const size_t need = sizeof(double) * (size_t)h->K * h->n;
@@ -1483,6 +1583,7 @@ psp_status psp_estimate_rho(psp_handle h, int32_t w, int32_t max_iter, double rt
   if (!h || !v0_h || !rho_h || max_iter < 1 || !(rtol > 0)) return PSP_ERR_ARG;
   if (!h->factored || h->W == 0) return fail(h, PSP_ERR_STATE, "factor_batch and set_weights first");
   if (w < 0 || w >= h->W) return fail(h, PSP_ERR_ARG, "w out of range");
+  if (h->transversal) return fail(h, PSP_ERR_UNSUPPORTED, "psp_estimate_rho with PSP_OPT_TRANSVERSAL");
   const int32_t n = h->n;
   cudaSetDevice(h->device);
   psp_status s;
@@ -1512,7 +1613,7 @@ psp_status psp_estimate_rho(psp_handle h, int32_t w, int32_t max_iter, double rt
     }
     CUDA_TRY(h, cudaMemcpyAsync(h->rho_r_d.p, r.data(), sizeof(double) * n, cudaMemcpyHostToDevice,
                                 h->stream));
-    if ((s = psp_solve_batch(h, 1, (const double*)h->rho_r_d.p, n))) return s;
+    if ((s = solve_impl(h, 1, (const double*)h->rho_r_d.p, n))) return s;
     if ((s = psp_recover(h, (double*)h->rho_x_d.p))) return s;
     CUDA_TRY(h, cudaMemcpyAsync(u.data(), (const double*)h->rho_x_d.p + (size_t)w * n,
                                 sizeof(double) * n, cudaMemcpyDeviceToHost, h->stream));
@@ -1602,6 +1703,13 @@ psp_status psp_get_factor(psp_handle h, int32_t k, double* vals_h) {
   return PSP_OK;
 }
 
+psp_status psp_get_transversal(psp_handle h, int32_t* q_h) {
+  if (!h || !q_h) return PSP_ERR_ARG;
+  if (!h->analysed || !h->transversal) return fail(h, PSP_ERR_STATE, "analyse with PSP_OPT_TRANSVERSAL = 1 first");
+  std::copy(h->tq.begin(), h->tq.end(), q_h);
+  return PSP_OK;
+}
+
 psp_status psp_get_dense_factor(psp_handle h, int32_t k, double* lu_h) {
   if (!h || !lu_h) return PSP_ERR_ARG;
   if (!h->factored || !h->dense_factored) return fail(h, PSP_ERR_STATE, "dense factor_batch first");
@@ -1619,6 +1727,7 @@ psp_status psp_set_perturbation_matrix(psp_handle h, const double* D_h) {
   if (!h) return PSP_ERR_ARG;
   if (h->device < 0) return fail(h, PSP_ERR_UNSUPPORTED, "host-only handle (device < 0)");
   if (!h->analysed) return fail(h, PSP_ERR_STATE, "psp_symbolic_analyse first");
+  if (D_h && h->transversal) return fail(h, PSP_ERR_UNSUPPORTED, "a dense D with PSP_OPT_TRANSVERSAL");
   cudaSetDevice(h->device);
   CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   if (!D_h) {
@@ -1777,6 +1886,9 @@ psp_status psp_residual(psp_handle h, const double* A_vals, int32_t W, int32_t R
   if (!h->rowptr_d) return fail(h, PSP_ERR_STATE, "symbolic_analyse first");
   cudaSetDevice(h->device);
   psp_status s;
+  int64_t ldb = h->n;
+  if ((s = tv_A(h, A_vals, 1))) return s;   // (||A_hat x - b_hat|| = ||A x - b||)
+  if ((s = tv_B(h, B, R, ldb))) return s;
   if ((s = ensure(h, h->res_d, sizeof(double) * (size_t)W * R))) return s;
   CUDA_TRY(h, psp::launch_residual(h->n, h->rowptr_d, h->colidx_d, A_vals, W, R, B, x,
                                    (double*)h->res_d.p, h->stream));

@@ -170,6 +170,12 @@ cudaError_t launch_recover_seg(const DevicePlan& p, int32_t W, int32_t R, const 
 cudaError_t launch_refine_step(const DevicePlan& p, int32_t K, const int32_t* row_ptr, const int32_t* col_idx,
                                const double* A, const double* b, const double* x, double* r, cudaStream_t stream);
 cudaError_t launch_refine_update(const DevicePlan& p, int32_t K, const double* X, double* x, cudaStream_t stream);
+// Structural transversal: dst[j][q'] = src[j * nnz + amap[q']] (n_jac value arrays), and
+// dst[(j R + r) n + i] = src[j * jac_stride + r * ldb + q[i]] (compact B_hat, ldb' = n).
+cudaError_t launch_gather_a(const int32_t* amap, int32_t nnz, int32_t n_jac, const double* src, double* dst,
+                            cudaStream_t stream);
+cudaError_t launch_gather_b(const int32_t* q, int32_t n, int32_t R, int32_t n_jac, const double* src, int64_t ldb,
+                            int64_t jac_stride, double* dst, cudaStream_t stream);
 cudaError_t launch_gather_solutions(const DevicePlan& p, int32_t K, int32_t R, const double* X,
                                     double* out, cudaStream_t stream);
 

@@ -33,6 +33,84 @@
 
 namespace psp {
 
+// Hopcroft-Karp maximum matching columns -> rows (the structural transversal of P:L304),
+// every choice in a fixed order (R20): per phase a BFS from the free columns in
+// ascending order (rows of a column ascending) computes layer distances, NIL standing for a
+// free row; then a DFS from each free column in ascending order along layered edges (an
+// explicit stack in the order the recursive form visits).  q[j] = row matched to column j,
+// -1 if none.  O(nnz sqrt(n)).
+std::vector<int32_t> transversal_hk(int32_t n, const int32_t* row_ptr, const int32_t* col_idx) {
+  std::vector<int32_t> cptr(n + 1, 0), crow(row_ptr[n]);
+  for (int32_t q = 0; q < row_ptr[n]; ++q) ++cptr[col_idx[q] + 1];
+  for (int32_t j = 0; j < n; ++j) cptr[j + 1] += cptr[j];
+  {
+    std::vector<int32_t> fill(cptr.begin(), cptr.end() - 1);
+    for (int32_t i = 0; i < n; ++i)   // rows ascending within each column
+      for (int32_t q = row_ptr[i]; q < row_ptr[i + 1]; ++q) crow[fill[col_idx[q]]++] = i;
+  }
+  const int32_t kInf = INT32_MAX;
+  std::vector<int32_t> col_match(n, -1), row_match(n, -1), dist(n), queue;
+  std::vector<std::pair<int32_t, int32_t>> stk;   // (column, position in its row list)
+  for (;;) {
+    queue.clear();
+    for (int32_t j = 0; j < n; ++j) {
+      if (col_match[j] < 0) {
+        dist[j] = 0;
+        queue.push_back(j);
+      } else {
+        dist[j] = kInf;
+      }
+    }
+    int32_t dnil = kInf;
+    for (size_t h = 0; h < queue.size(); ++h) {
+      const int32_t j = queue[h];
+      if (dist[j] >= dnil) continue;
+      for (int32_t t = cptr[j]; t < cptr[j + 1]; ++t) {
+        const int32_t j2 = row_match[crow[t]];
+        if (j2 < 0) {
+          if (dnil == kInf) dnil = dist[j] + 1;
+        } else if (dist[j2] == kInf) {
+          dist[j2] = dist[j] + 1;
+          queue.push_back(j2);
+        }
+      }
+    }
+    if (dnil == kInf) break;
+    for (int32_t j0 = 0; j0 < n; ++j0) {
+      if (col_match[j0] >= 0) continue;
+      stk.assign(1, {j0, cptr[j0]});
+      while (!stk.empty()) {
+        auto& top = stk.back();
+        const int32_t j = top.first;
+        if (top.second == cptr[j + 1]) {   // no augmenting path through j
+          dist[j] = kInf;
+          stk.pop_back();
+          if (!stk.empty()) ++stk.back().second;
+          continue;
+        }
+        const int32_t i = crow[top.second];
+        const int32_t j2 = row_match[i];
+        if (j2 < 0) {
+          if (dnil == dist[j] + 1) {   // augment along the stack
+            for (const auto& f : stk) {
+              const int32_t r = crow[f.second];
+              col_match[f.first] = r;
+              row_match[r] = f.first;
+            }
+            break;
+          }
+          ++top.second;
+        } else if (dist[j2] == dist[j] + 1) {
+          stk.push_back({j2, cptr[j2]});
+        } else {
+          ++top.second;
+        }
+      }
+    }
+  }
+  return col_match;
+}
+
 std::vector<int32_t> min_degree_order(int32_t n, const std::vector<std::vector<int32_t>>& adj0,
                                       int32_t first) {
   std::vector<std::vector<int32_t>> adj = adj0;  // sorted neighbour lists

@@ -81,6 +81,7 @@ void build_coop(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
                 const std::vector<int32_t>& perm, const int32_t* row_ptr_h,
                 const int32_t* col_idx_h, const HostPlan& P, CoopPlan& C);
 
+std::vector<int32_t> transversal_hk(int32_t n, const int32_t* row_ptr, const int32_t* col_idx);
 std::vector<int32_t> min_degree_order(int32_t n, const std::vector<std::vector<int32_t>>& adj,
                                       int32_t first);
 EtreeResult symbolic_etree(int32_t n, const std::vector<std::vector<int32_t>>& adjp);

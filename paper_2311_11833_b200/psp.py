@@ -15,7 +15,8 @@ LIB_PATH = os.environ.get("PSP_LIB", os.path.join(_HERE, "libpsp.so"))
 PSP_OK = 0
 STATUS = {0: "PSP_OK", 1: "PSP_ERR_ARG", 2: "PSP_ERR_DIM", 3: "PSP_ERR_STATE",
           4: "PSP_ERR_ZERO_PIVOT", 5: "PSP_ERR_BATCH_INFEASIBLE", 6: "PSP_ERR_CUDA",
-          7: "PSP_ERR_ALLOC", 8: "PSP_ERR_UNSUPPORTED", 9: "PSP_ERR_NCCL"}
+          7: "PSP_ERR_ALLOC", 8: "PSP_ERR_UNSUPPORTED", 9: "PSP_ERR_NCCL",
+          10: "PSP_ERR_STRUCT_SINGULAR"}
 PSP_ERR_ZERO_PIVOT = 4
 PSP_ERR_BATCH_INFEASIBLE = 5
 ORDER = {"natural": 0, "mindeg": 1, "user": 2, "mindeg_first": 3}
@@ -30,12 +31,13 @@ EXPORTS = ["psp_create", "psp_destroy", "psp_set_stream", "psp_status_string",
            "psp_get_unique_id", "psp_comm_init", "psp_set_perturbations_shard", "psp_shard_weights",
            "psp_set_weights_dense", "psp_recover_reduce", "psp_get_dense_factor",
            "psp_set_perturbation_matrix", "psp_factor_batch_multi", "psp_solve_batch_multi",
-           "psp_refine"]
+           "psp_refine", "psp_get_transversal"]
 KERNEL = {0: "none", 1: "coop", 2: "batch", 3: "batch_tmem", 4: "batch_spill", 5: "dense", 6: "coop_global"}
 PATH = {"sparse": 0, "dense": 1}
 OPT = {"factor_groups": 1, "factor_warps": 2, "factor_lanes": 3, "factor_slab_warps": 4,
        "factor_pairs": 5, "factor_tmem": 6, "solve_tmem": 7, "phase_events": 8, "growth": 9, "coop": 10,
-       "factor_spill": 11, "path": 12, "coop_global": 13}
+       "factor_spill": 11, "path": 12, "coop_global": 13,
+       "transversal": 14}
 
 
 class SymbolicInfo(ctypes.Structure):
@@ -113,6 +115,7 @@ def lib():
             "psp_factor_batch_multi": [P, I32, P, D, P],
             "psp_solve_batch_multi": [P, I32, P, I64, I64],
             "psp_refine": [P, P, P, I32, P],
+            "psp_get_transversal": [P, P],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -221,6 +224,12 @@ class Solver:
         self._check_dev(out, self.torch.float64, (self.K, self.n))
         self._check(lib().psp_refine(self.h, _t_ptr(A_vals), _t_ptr(b), int(iters), _t_ptr(out)))
         return out
+
+    def psp_get_transversal(self):
+        """The Hopcroft-Karp row matching q of the last analysis (PSP_OPT_TRANSVERSAL)."""
+        q = np.empty(self.n, dtype=np.int32)
+        self._check(lib().psp_get_transversal(self.h, _np_ptr(q)))
+        return q
 
     def psp_get_dense_factor(self, k):
         """Lane k's dense factor (host numpy n x n, permuted order; L strict lower, U upper)."""
@@ -517,6 +526,13 @@ class HostSymbolic:
         st = lib().psp_set_option(self.h, OPT[name], int(value))
         if st:
             raise PSPError(st, lib().psp_last_error_detail(self.h).decode())
+
+    def get_transversal(self, n):
+        q = np.empty(int(n), dtype=np.int32)
+        st = lib().psp_get_transversal(self.h, _np_ptr(q))
+        if st:
+            raise PSPError(st, lib().psp_last_error_detail(self.h).decode())
+        return q
 
     def analyse(self, n, row_ptr, col_idx, ordering="mindeg", user_perm=None, first_node=-1):
         rp = np.ascontiguousarray(row_ptr, dtype=np.int32)

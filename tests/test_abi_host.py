@@ -131,3 +131,50 @@ def test_options_validated_and_reported():
     info3, _ = hs.analyse(s.n, s.row_ptr, s.col_idx)
     assert info3["factor_pend_smem"] == 2 and info3["aug_max_live"] > info3["max_live"]
     hs.close()
+
+
+# --- structural transversal (PSP_OPT_TRANSVERSAL) --------------------------------
+def _hk_case(n, rp, ci):
+    from oracle import transversal
+    hs = psp.HostSymbolic()
+    hs.set_option("transversal", 1)
+    info, perm = hs.analyse(n, rp, ci)
+    q = hs.get_transversal(n)
+    qo = transversal.hopcroft_karp(n, rp, ci)
+    assert np.array_equal(q, np.array(qo, np.int32))        # bit-exact integer work
+    # the symmetric order is the oracle's min-degree order of A_hat = A[q, :]
+    trp, tci, _ = transversal.permuted_rows(n, rp, ci, np.ones(len(ci)), qo)
+    assert np.array_equal(perm, ordering.elimination_order(n, trp, tci))
+    return info
+
+
+@pytest.mark.parametrize("ci", [0, 1])
+def test_transversal_matches_oracle_on_listed_jacobian(ci):
+    s = config(ci).system(convention="listed")
+    info = _hk_case(s.n, s.row_ptr, s.col_idx)
+    assert info["n_struct_zero_diag"] == 0                    # zero-free diagonal after it
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_transversal_matches_oracle_random(seed):
+    rng = np.random.default_rng(seed)
+    n = 40
+    M = rng.random((n, n)) < 0.08
+    M[np.arange(n), np.arange(n)] &= rng.random(n) < 0.3        # few diagonal entries
+    M[np.arange(n), rng.permutation(n)] = True                  # structurally nonsingular
+    rp, ci = [0], []
+    for i in range(n):
+        ci.extend(np.flatnonzero(M[i]).tolist())
+        rp.append(len(ci))
+    _hk_case(n, np.array(rp, np.int32), np.array(ci, np.int32))
+
+
+def test_transversal_structurally_singular():
+    n = 4   # rows 0 and 1 both only in column 0
+    rp = np.array([0, 1, 2, 4, 6], np.int32)
+    ci = np.array([0, 0, 1, 2, 2, 3], np.int32)
+    hs = psp.HostSymbolic()
+    hs.set_option("transversal", 1)
+    with pytest.raises(psp.PSPError) as e:
+        hs.analyse(n, rp, ci)
+    assert e.value.status == 10
