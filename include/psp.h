@@ -160,6 +160,12 @@ psp_status psp_destroy(psp_handle h);
  *                         factor image lane-major in the handle's factor storage, the same
  *                         etree-level schedule: bitwise the batch kernels); 1: always (when
  *                         built: set before psp_symbolic_analyse); 2: never.  Bitwise-neutral.
+ *  PSP_OPT_DATAFLOW       1: psp_factor_solve_batch on a batch that takes the cooperative
+ *                         kernels runs ONE fused kernel instead: a CTA per system whose
+ *                         factor entries, forward rows and backward rows are dataflow tasks
+ *                         walked by one lane per warp (ready flags in shared memory, no level
+ *                         barriers); same arithmetic, bitwise; 0 (default): only for small
+ *                         systems (nnz_LU <= 1024, where it measured faster); 2: never.
  *  PSP_OPT_TRANSVERSAL    0 (default); 1: the structural pre-pass of P:L304 ("the
  *                         Hopcroft-Karp algorithm (which permutes a matrix by moving
  *                         non-zeros onto the diagonal)"): the analysis computes a maximum
@@ -191,7 +197,7 @@ enum { PSP_OPT_FACTOR_GROUPS = 1, PSP_OPT_FACTOR_WARPS = 2, PSP_OPT_FACTOR_LANES
        PSP_OPT_FACTOR_SLAB_WARPS = 4, PSP_OPT_FACTOR_PAIRS = 5, PSP_OPT_FACTOR_TMEM = 6,
        PSP_OPT_SOLVE_TMEM = 7, PSP_OPT_PHASE_EVENTS = 8, PSP_OPT_GROWTH = 9,
        PSP_OPT_COOP = 10, PSP_OPT_FACTOR_SPILL = 11, PSP_OPT_PATH = 12, PSP_OPT_COOP_GLOBAL = 13,
-       PSP_OPT_TRANSVERSAL = 14 };
+       PSP_OPT_TRANSVERSAL = 14, PSP_OPT_DATAFLOW = 15 };
 psp_status psp_set_option(psp_handle h, int32_t option, int64_t value);
 
 /* Rebind the handle to another stream of the same device.  Synchronises the old stream
@@ -348,8 +354,9 @@ enum { PSP_KERNEL_NONE = 0,
        PSP_KERNEL_BATCH_SPILL = 4, /* batch factor, capacity-planned slots (TMEM + shared)
                                       with idle entries spilled to global memory            */
        PSP_KERNEL_DENSE = 5,       /* dense path (PSP_OPT_PATH): blocked LU / solves, DMMA   */
-       PSP_KERNEL_COOP_GLOBAL = 6  /* level-scheduled CTA per system, factor image in global
+       PSP_KERNEL_COOP_GLOBAL = 6, /* level-scheduled CTA per system, factor image in global
                                       memory (large n, PSP_OPT_COOP_GLOBAL)                  */
+       PSP_KERNEL_DATAFLOW = 7     /* fused factor + solve by dataflow (PSP_OPT_DATAFLOW)     */
 };
 psp_status psp_get_last_kernels(psp_handle h, int32_t* kernels_h);
 

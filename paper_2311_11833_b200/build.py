@@ -7,7 +7,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpsp.so")
-SOURCES = ["psp_host.cpp", "psp_plan.cpp", "psp_kernels.cu", "psp_dense.cu", "psp_coopg.cu"]
+SOURCES = ["psp_host.cpp", "psp_plan.cpp", "psp_kernels.cu", "psp_dense.cu", "psp_coopg.cu", "psp_dataflow.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

@@ -22,6 +22,7 @@
 #include "../../include/psp.h"
 #include "psp_internal.h"
 #include "psp_coopg.h"
+#include "psp_dataflow.h"
 #include "psp_dense.h"
 #include "psp_plan.h"
 
@@ -101,6 +102,12 @@ struct psp_ctx {
   psp::CoopDev coop;
   bool coop_ok = false;
   int64_t opt_coop = 0;            // PSP_OPT_COOP: 0 automatic (K <= 8 * SMs), 1 on, 2 off
+  // fused factor + solve by dataflow (psp_dataflow.cu): the small-batch, one-RHS latency path
+  bool df_ok = false;
+  int64_t opt_df = 0;              // PSP_OPT_DATAFLOW: 0 automatic (with the coop kernels), 1 on, 2 off
+  const uint32_t* df_plan = nullptr;
+  int32_t df_words = 0;
+  size_t df_smem = 0;
   // level-scheduled kernels for large systems (CTA per system, factor image lane-major in
   // V_d: psp_coopg.cu), used when the cooperative kernels' shared-memory image does not fit
   psp::CoopGDev coopg;
@@ -430,6 +437,10 @@ psp_status psp_set_option(psp_handle h, int32_t option, int64_t value) {
       if (value != 0 && value != 1 && value != 2)
         return fail(h, PSP_ERR_ARG, "PSP_OPT_FACTOR_SLAB_WARPS must be 0, 1 or 2");
       h->opt_slab_warps = value;
+      return PSP_OK;
+    case PSP_OPT_DATAFLOW:
+      if (value < 0 || value > 2) return fail(h, PSP_ERR_ARG, "PSP_OPT_DATAFLOW must be 0, 1 or 2");
+      h->opt_df = value;
       return PSP_OK;
     case PSP_OPT_TRANSVERSAL:
       if (value != 0 && value != 1) return fail(h, PSP_ERR_ARG, "PSP_OPT_TRANSVERSAL must be 0 or 1");
@@ -795,6 +806,23 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
       c = psp::CoopDev{};
     }
   }
+  h->df_ok = false;
+  h->df_plan = nullptr;
+  if (!host_only && h->coop_ok && h->opt_df != 2) {
+    psp::DataflowPlan DF;
+    psp::build_dataflow(n, S.lcol, HP, psp::kDfWorkers, DF);
+    const size_t smem = DF.ok ? psp::dataflow_smem(HP.nnz_LU, n, (int)DF.words.size()) : 0;
+    if (DF.ok && smem <= (size_t)(227 * 1024 - 64)) {
+      if ((s = upload(h, DF.words, &h->df_plan))) return s;
+      h->df_words = (int32_t)DF.words.size();
+      h->df_smem = smem;
+      if (psp::configure_dataflow(smem) == cudaSuccess) {
+        h->df_ok = true;
+      } else {
+        cudaGetLastError();
+      }
+    }
+  }
   h->coopg_ok = false;
   h->coopg = psp::CoopGDev{};
   if (!host_only && h->opt_coopg != 2 && (!h->coop_ok || h->opt_coopg == 1)) {
@@ -1113,6 +1141,63 @@ static bool use_spill(psp_ctx* h, bool aug) {
 
 static psp_status solve_impl(psp_handle h, int32_t R, const double* B, int64_t ldb);
 
+// Fused factor + forward + backward for one right-hand side by dataflow (psp_dataflow.cu):
+// the small-batch latency path; bitwise the coop factor + solve.
+static psp_status dataflow_factor_solve(psp_handle h, const double* A_vals, const double* b, double pivot_tol,
+                                        int32_t* lane_status) {
+  if (!A_vals) return fail(h, PSP_ERR_ARG, "A_vals required");
+  if (!(pivot_tol == pivot_tol)) return fail(h, PSP_ERR_ARG, "pivot_tol is NaN");
+  cudaSetDevice(h->device);
+  psp_status s;
+  const size_t need = sizeof(double) * (size_t)h->K_pad * h->n;
+  if (h->X_d.bytes < need) {
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    if ((s = ensure(h, h->X_d, need))) return s;
+  }
+  psp::DataflowArgs a;
+  a.n = h->n;
+  a.nnz_LU = h->nnz_LU;
+  a.LS = kBlock / h->launch.f_groups * h->launch.f_lanes;
+  a.plan = h->df_plan;
+  a.plan_words = h->df_words;
+  a.birth_src = h->coop.birth_src;
+  a.birth_diag = h->coop.birth_diag;
+  a.perm = h->plan.perm;
+  a.A = A_vals;
+  a.eps = (const double*)h->eps_d.p;
+  a.dperm = (const double*)h->dperm_d.p;
+  a.b = b;
+  if (pivot_tol <= 0) {
+    CUDA_TRY(h, psp::launch_pivot_tol(h->plan, A_vals, (double*)h->tol_d.p, h->stream));
+    a.tol_dev = (const double*)h->tol_d.p;
+  }
+  a.tol_value = pivot_tol;
+  a.V = (double*)h->V_d.p;
+  a.X = (double*)h->X_d.p;
+  a.status = (int32_t*)h->status_d.p;
+  if (h->phase_events) {
+    if ((s = phase_mark(h, h->fev, h->nf))) return s;
+  }
+  CUDA_TRY(h, psp::launch_dataflow(a, h->K, h->df_smem, h->stream));
+  if (h->phase_events) {
+    if ((s = phase_mark(h, h->fev, h->nf))) return s;
+  }
+  h->last_factor = h->last_solve = PSP_KERNEL_DATAFLOW;
+  h->last_factor_aug = 1;
+  h->last_solve_fwd = 0;
+  h->growth_valid = false;
+  if (lane_status)
+    CUDA_TRY(h, cudaMemcpyAsync(lane_status, h->status_d.p, sizeof(int32_t) * h->K,
+                                cudaMemcpyDeviceToDevice, h->stream));
+  h->factored = true;
+  h->dense_factored = h->coopg_factored = false;
+  h->mj = psp::MultiJac{};
+  h->R = 1;
+  h->solved = true;
+  h->recovered = false;
+  return PSP_OK;
+}
+
 // Dense path (psp_dense.cu): K padded N x N factors, one CTA per lane.
 static psp_status dense_factor(psp_handle h, const double* A_vals, double pivot_tol,
                                int32_t* lane_status, psp::MultiJac mj = psp::MultiJac{}) {
@@ -1398,6 +1483,12 @@ psp_status psp_factor_solve_batch(psp_handle h, const double* A_vals, const doub
     if ((s = tv_A(h, A_vals, 1))) return s;
     if ((s = tv_B(h, b, 1, ldb))) return s;
   }
+  // (automatic only for small systems: measured on the B200, cfg0 (nnz_LU = 2.3e2) 28.7 us vs
+  // 40.0 us per step for the cooperative factor + solve, but cfg1 (5.5e3) 330 vs 135 us --
+  // the walkers' per-contribution flag checks cost more than the barriers they replace)
+  if (h->analysed && h->K > 0 && h->opt_path != PSP_PATH_DENSE && !h->dense_D && use_coop(h) && h->df_ok &&
+      (h->opt_df == 1 || (h->opt_df == 0 && h->nnz_LU <= 1024)) && !h->growth)
+    return dataflow_factor_solve(h, A_vals, b, pivot_tol, lane_status);
   if (h->analysed && (h->opt_path == PSP_PATH_DENSE || use_coopg(h))) {
     if ((s = factor_impl(h, A_vals, pivot_tol, lane_status, false, nullptr))) return s;
     return solve_impl(h, 1, b, h->n);

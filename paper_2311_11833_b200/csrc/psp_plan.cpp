@@ -434,6 +434,126 @@ void build_coop(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
   }
 }
 
+void build_dataflow(int32_t n, const std::vector<std::vector<int32_t>>& lcol, const HostPlan& P,
+                    int32_t threads, DataflowPlan& D) {
+  D = DataflowPlan{};
+  const int32_t nnzL = P.nnz_L, nnzLU = P.nnz_LU;
+  if (nnzLU >= 0xffff || n >= 0xffff) return;
+  auto pos_in = [&](int32_t col, int32_t row) -> int32_t {
+    const auto& v = lcol[col];
+    return (int32_t)(std::lower_bound(v.begin(), v.end(), row) - v.begin());
+  };
+  auto pos = [&](int32_t i, int32_t j) -> int32_t {   // V-image position of entry (i, j)
+    if (i == j) return nnzL + P.dofs[i];
+    if (i > j) return P.lofs[j] + pos_in(j, i);
+    return nnzL + P.dofs[i] + 1 + pos_in(i, j);
+  };
+  // task ids: factor entry t -> t; forward row i -> nnzLU + i; backward row i -> nnzLU + n + i
+  const int32_t nt = nnzLU + 2 * n;
+  std::vector<std::vector<std::pair<int32_t, int32_t>>> con(nt);   // (a, b) operand ids
+  std::vector<int32_t> entry_i(nnzLU), entry_j(nnzLU);
+  for (int32_t p = 0; p < n; ++p) {
+    entry_i[pos(p, p)] = entry_j[pos(p, p)] = p;
+    for (int32_t i : lcol[p]) {
+      entry_i[pos(i, p)] = i; entry_j[pos(i, p)] = p;
+      entry_i[pos(p, i)] = p; entry_j[pos(p, i)] = i;
+    }
+  }
+  // factor: entry (a, b) of pivot p's block receives (l_ap, u_pb), p ascending
+  for (int32_t p = 0; p < n; ++p) {
+    const auto& L = lcol[p];
+    for (int32_t a : L)
+      for (int32_t b : L) con[pos(a, b)].push_back({pos(a, p), pos(p, b)});
+  }
+  // forward: y_i receives (l_ip, y_p), p ascending; backward: x_i receives (u_ik, x_k), k descending
+  for (int32_t p = 0; p < n; ++p)
+    for (int32_t i : lcol[p]) con[nnzLU + i].push_back({pos(i, p), p});
+  for (int32_t i = 0; i < n; ++i)
+    for (int32_t k = (int32_t)lcol[i].size() - 1; k >= 0; --k) con[nnzLU + n + i].push_back({pos(i, lcol[i][k]), lcol[i][k]});
+  // ASAP schedule: the earliest finish time of every task with unit cost per contribution
+  // (an operand pair's wait + one fma) and 3 for a division; a contribution starts when
+  // the task's previous one is done and both operands are final.  Tasks are then dealt to
+  // the threads round-robin in order of their earliest finish, so that every thread walks
+  // its tasks in the order an ideal schedule completes them.  (Kinds in id order are topologically ordered: factor
+  // entries by their smaller index, diagonals first; forward rows ascending; backward
+  // rows descending.)
+  std::vector<int32_t> fin(nt, 0), start(nt, 0);
+  std::vector<int32_t> order(nnzLU);
+  for (int32_t t = 0; t < nnzLU; ++t) order[t] = t;
+  std::vector<int32_t> diag_of(nnzLU, -1);
+  for (int32_t t = 0; t < nnzLU; ++t)
+    if (entry_i[t] > entry_j[t]) diag_of[t] = pos(entry_j[t], entry_j[t]);
+  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+    const int32_t ma = std::min(entry_i[a], entry_j[a]), mb = std::min(entry_i[b], entry_j[b]);
+    if (ma != mb) return ma < mb;
+    return (entry_i[a] == entry_j[a]) > (entry_i[b] == entry_j[b]);
+  });
+  auto run = [&](int32_t t, int32_t t0, auto&& ready_a, auto&& ready_b) {
+    int32_t clk = t0, first = -1;
+    for (auto& c : con[t]) {
+      clk = std::max({clk, ready_a(c.first), ready_b(c.second)}) + 1;
+      if (first < 0) first = clk - 1;
+    }
+    start[t] = first < 0 ? t0 : first;
+    return clk;
+  };
+  auto fe = [&](int32_t e) { return fin[e]; };
+  for (int32_t t : order) {
+    int32_t clk = run(t, 0, fe, fe);
+    if (diag_of[t] >= 0) clk = std::max(clk, fin[diag_of[t]]) + 3;
+    fin[t] = clk;
+  }
+  auto fy = [&](int32_t i) { return fin[nnzLU + i]; };
+  auto fx = [&](int32_t i) { return fin[nnzLU + n + i]; };
+  for (int32_t i = 0; i < n; ++i) fin[nnzLU + i] = run(nnzLU + i, 0, fe, fy);
+  for (int32_t i = n - 1; i >= 0; --i) {
+    const int32_t t = nnzLU + n + i;
+    const int32_t clk = run(t, fin[nnzLU + i], fe, fx);
+    fin[t] = std::max(clk, fin[pos(i, i)]) + 3;
+  }
+  std::vector<int32_t> all(nt);
+  for (int32_t t = 0; t < nt; ++t) all[t] = t;
+  // (by finish time: every dependency finishes strictly earlier, so each thread's list is
+  // topologically ordered -- the unfinished task of least finish time can always proceed)
+  std::stable_sort(all.begin(), all.end(), [&](int32_t a, int32_t b) {
+    return fin[a] != fin[b] ? fin[a] < fin[b] : start[a] < start[b];
+  });
+  for (auto& c : con)
+    if (c.size() >= (1u << 13)) return;
+  std::vector<std::vector<uint32_t>> seg(threads);
+  for (int32_t r = 0; r < nt; ++r) {
+    const int32_t t = all[r];
+    auto& w = seg[r % threads];
+    const uint32_t cnt = (uint32_t)con[t].size();
+    if (t < nnzLU) {   // F: [0 | isdiag << 29 | cnt << 16 | p], [t | diag << 16]
+      const bool isd = entry_i[t] == entry_j[t];
+      w.push_back((0u << 30) | ((isd ? 1u : 0u) << 29) | (cnt << 16) | (uint32_t)entry_i[t]);
+      w.push_back((uint32_t)t | ((diag_of[t] >= 0 ? (uint32_t)diag_of[t] : 0xffffu) << 16));
+    } else if (t < nnzLU + n) {   // Y: [1 << 30 | cnt << 16], [i]
+      w.push_back((1u << 30) | (cnt << 16));
+      w.push_back((uint32_t)(t - nnzLU) | (0xffffu << 16));
+    } else {   // X: [2 << 30 | cnt << 16], [i | u_ii position << 16]
+      const int32_t i = t - nnzLU - n;
+      w.push_back((2u << 30) | (cnt << 16));
+      w.push_back((uint32_t)i | ((uint32_t)pos(i, i) << 16));
+    }
+    for (auto& c : con[t]) w.push_back((uint32_t)c.first | ((uint32_t)c.second << 16));
+  }
+  D.words.assign(threads + 1, 0);
+  for (int32_t th = 0; th < threads; ++th) {
+    D.words[th + 1] = D.words[th] + (uint32_t)seg[th].size();
+  }
+  const uint32_t base = (uint32_t)threads + 1;
+  for (int32_t th = 0; th <= threads; ++th) D.words[th] += base;
+  for (auto& sgm : seg) D.words.insert(D.words.end(), sgm.begin(), sgm.end());
+  while (D.words.size() % 4) D.words.push_back(0);
+  D.threads = threads;
+  D.tasks = nt;
+  D.depth = 0;
+  for (int32_t t = 0; t < nt; ++t) D.depth = std::max(D.depth, fin[t]);
+  D.ok = true;
+}
+
 void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
                     const std::vector<int32_t>& perm, const int32_t* row_ptr_h,
                     const int32_t* col_idx_h, HostPlan& P) {

@@ -81,6 +81,18 @@ void build_coop(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
                 const std::vector<int32_t>& perm, const int32_t* row_ptr_h,
                 const int32_t* col_idx_h, const HostPlan& P, CoopPlan& C);
 
+// Dataflow plan of the fused small-batch factor + solve (psp_dataflow.cu): every factor
+// entry, forward row and backward row is a task with its contributions in canonical order;
+// tasks sorted by dependency depth and dealt round-robin to the CTA's threads.  Packed
+// 16-bit fields (ok = false when positions or counts do not fit).  words: [threads + 1]
+// segment offsets, then the records (see psp_dataflow.cu).
+struct DataflowPlan {
+  bool ok = false;
+  int32_t threads = 0, depth = 0, tasks = 0;
+  std::vector<uint32_t> words;
+};
+void build_dataflow(int32_t n, const std::vector<std::vector<int32_t>>& lcol, const HostPlan& P,
+                    int32_t threads, DataflowPlan& D);
 std::vector<int32_t> transversal_hk(int32_t n, const int32_t* row_ptr, const int32_t* col_idx);
 std::vector<int32_t> min_degree_order(int32_t n, const std::vector<std::vector<int32_t>>& adj,
                                       int32_t first);

@@ -32,12 +32,12 @@ EXPORTS = ["psp_create", "psp_destroy", "psp_set_stream", "psp_status_string",
            "psp_set_weights_dense", "psp_recover_reduce", "psp_get_dense_factor",
            "psp_set_perturbation_matrix", "psp_factor_batch_multi", "psp_solve_batch_multi",
            "psp_refine", "psp_get_transversal"]
-KERNEL = {0: "none", 1: "coop", 2: "batch", 3: "batch_tmem", 4: "batch_spill", 5: "dense", 6: "coop_global"}
+KERNEL = {0: "none", 1: "coop", 2: "batch", 3: "batch_tmem", 4: "batch_spill", 5: "dense", 6: "coop_global", 7: "dataflow"}
 PATH = {"sparse": 0, "dense": 1}
 OPT = {"factor_groups": 1, "factor_warps": 2, "factor_lanes": 3, "factor_slab_warps": 4,
        "factor_pairs": 5, "factor_tmem": 6, "solve_tmem": 7, "phase_events": 8, "growth": 9, "coop": 10,
        "factor_spill": 11, "path": 12, "coop_global": 13,
-       "transversal": 14}
+       "transversal": 14, "dataflow": 15}
 
 
 class SymbolicInfo(ctypes.Structure):
