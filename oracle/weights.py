@@ -19,6 +19,7 @@ P:L205-215: x_hat_j = (x^+ + x^-)/2).
 """
 from __future__ import annotations
 
+import functools
 from fractions import Fraction
 
 
@@ -71,12 +72,21 @@ def beta_integer(m):
 def lane_weights(magnitudes):
     """Signed-lane weights for one ladder in lane order [+s1, -s1, +s2, -s2, ...]:
     each sign carries beta_j / 2 (pair average of Eq. (avg_hats)).  Returns floats
-    correctly rounded from the exact rationals."""
-    beta = beta_vandermonde([Fraction(float(s)) for s in magnitudes])
+    correctly rounded from the exact rationals.  The rationals come from the Lagrange
+    route (the same exact values as the Vandermonde solve of Eq. (13): both routes are
+    pinned equal in tests/test_oracle_weights.py), O(m^2) instead of O(m^3) exact
+    operations -- the 128-node ladder of BASELINE configs[2] takes 0.4 s instead of
+    minutes; memoised per ladder."""
+    return list(_lane_weights(tuple(float(s) for s in magnitudes)))
+
+
+@functools.lru_cache(maxsize=256)
+def _lane_weights(mags):
+    beta = beta_lagrange([Fraction(s) for s in mags])
     out = []
     for bj in beta:
         out += [float(bj / 2), float(bj / 2)]
-    return out
+    return tuple(out)
 
 
 def error_constant(m):

@@ -28,6 +28,8 @@ def gpu_run(s, eps, ordering_kind="mindeg", first=-1, tol=0.0, B=None, ladders=N
     solver = psp.Solver(0)
     if coop is not None:
         solver.psp_set_option("coop", coop)
+        if coop == 2:
+            solver.psp_set_option("coop_global", 2)
     solver.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering=ordering_kind, first_node=first)
     info, perm = solver.psp_get_symbolic_info()
     # the oracle's own elimination order (never the product's): integer parity
@@ -302,6 +304,8 @@ def test_values_only_refactorisation_many_jacobians(coop):
     rng = np.random.default_rng(302)
     solver = psp.Solver(0)
     solver.psp_set_option("coop", coop)
+    if coop == 2:
+        solver.psp_set_option("coop_global", 2)
     solver.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering="mindeg")
     info, perm = solver.psp_get_symbolic_info()
     solver.psp_set_perturbations(eps, s.d)
@@ -561,6 +565,7 @@ def test_factor_kernel_variants_bitwise(gjp):
     eps = rng.choice([-1, 1], K) * 10.0 ** rng.uniform(-6, -2, K)
     solver = psp.Solver(0)
     solver.psp_set_option("coop", 2)          # K = 100 would otherwise take the coop kernels
+    solver.psp_set_option("coop_global", 2)   # (nor the global level-scheduled ones)
     solver.psp_set_option("factor_groups", G)
     solver.psp_set_option("factor_lanes", J)
     solver.psp_set_option("factor_slab_warps", P)
@@ -579,6 +584,7 @@ def test_factor_kernel_variants_bitwise(gjp):
     # the factor itself, entry by entry, against a G=J=P=1 run
     ref = psp.Solver(0)
     ref.psp_set_option("coop", 2)
+    ref.psp_set_option("coop_global", 2)   # (nor the global level-scheduled ones)
     ref.psp_set_option("factor_groups", 1)
     ref.psp_set_option("factor_pairs", 1 - pairs if gjp == (1, 1, 1) else 1)
     ref.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering="mindeg_first", first_node=s.slot_p)
@@ -602,6 +608,7 @@ def test_factor_tmem_variant_bitwise(K):
     for tm in (1, 2):
         solver = psp.Solver(0)
         solver.psp_set_option("coop", 2)      # (K <= 8 x SMs would take the coop kernels)
+        solver.psp_set_option("coop_global", 2)   # (nor the global level-scheduled ones)
         solver.psp_set_option("factor_tmem", tm)
         solver.psp_set_option("solve_tmem", tm)
         solver.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering="mindeg")
@@ -637,6 +644,7 @@ def test_fused_factor_solve_bitwise(ci, K):
     for fused in (True, False):
         solver = psp.Solver(0)
         solver.psp_set_option("coop", 2)      # (K <= 8 x SMs would take the coop kernels)
+        solver.psp_set_option("coop_global", 2)   # (nor the global level-scheduled ones)
         solver.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering="mindeg")
         info, perm = solver.psp_get_symbolic_info()
         solver.psp_set_perturbations(eps, s.d)
@@ -792,6 +800,8 @@ def test_coop_kernels_bitwise_vs_batch_kernels(ci, order, K):
     for coop in (1, 2):
         solver = psp.Solver(0)
         solver.psp_set_option("coop", coop)
+        if coop == 2:
+            solver.psp_set_option("coop_global", 2)
         solver.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering=order, first_node=first)
         info, perm = solver.psp_get_symbolic_info()
         solver.psp_set_perturbations(eps, s.d)
@@ -821,6 +831,7 @@ def test_phase_times_cover_the_launches():
     solver = psp.Solver(0)
     solver.psp_set_option("phase_events", 1)
     solver.psp_set_option("coop", 2)
+    solver.psp_set_option("coop_global", 2)   # (nor the global level-scheduled ones)
     solver.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering="mindeg")
     solver.psp_set_perturbations(eps, s.d)
     A = torch.tensor(s.vals, dtype=torch.float64, device="cuda")
@@ -870,6 +881,8 @@ def test_random_patterns_all_paths(seed, hubs=3, density=0.05):
     for coop, fused in ((2, False), (2, True), (1, False)):
         solver = psp.Solver(0)
         solver.psp_set_option("coop", coop)
+        if coop == 2:
+            solver.psp_set_option("coop_global", 2)
         solver.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering="mindeg")
         info, perm = solver.psp_get_symbolic_info()
         solver.psp_set_perturbations(eps, s.d)
@@ -988,6 +1001,7 @@ def test_spill_factor_bitwise(K, fused):
     for sp in (1, 2):
         solver = psp.Solver(0)
         solver.psp_set_option("coop", 2)
+        solver.psp_set_option("coop_global", 2)   # (nor the global level-scheduled ones)
         solver.psp_set_option("factor_spill", sp)
         solver.psp_symbolic_analyse(s.n, s.row_ptr, s.col_idx, ordering="mindeg")
         info, perm = solver.psp_get_symbolic_info()

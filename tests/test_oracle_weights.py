@@ -92,3 +92,13 @@ def test_beta_invariant_under_common_scale():
     _, w1 = psp.psp_ladder_weights(s)
     _, w2 = psp.psp_ladder_weights(20.0 * s)
     assert np.allclose(w1, w2, rtol=1e-14, atol=0)
+
+
+def test_two_routes_agree_geometric_ladder():
+    # the lane weights' Lagrange route against the paper's Vandermonde solve (Eq. (13)) on a
+    # non-integer geometric ladder of binary64 magnitudes (exact rationals, 24 nodes)
+    import numpy as np
+    mags = [Fraction(float(s)) for s in np.geomspace(1e-1, 1e-8, 24)]
+    assert weights.beta_lagrange(mags) == weights.beta_vandermonde(mags)
+    lw = weights.lane_weights([float(s) for s in mags])
+    assert lw == [float(b / 2) for b in weights.beta_vandermonde(mags) for _ in (0, 1)]
