@@ -105,12 +105,14 @@ __global__ void __launch_bounds__(kCgThreads, 4) coopg_factor_kernel(const __gri
 __global__ void __launch_bounds__(kCgThreads, 4) coopg_solve_kernel(const __grid_constant__ CoopGSolveArgs a) {
   const CoopGDev& c = a.c;
   extern __shared__ double y[];   // [n]
-  const int k = blockIdx.x, tid = threadIdx.x;
+  // one CTA per (lane, right-hand side): the R solves of a lane run in parallel, sharing
+  // (reading) the lane's factor image
+  const int k = blockIdx.x / a.R, r = blockIdx.x - k * a.R, tid = threadIdx.x;
   const double* __restrict__ v = a.W + (size_t)k * c.nnz_LU;
   auto vg = [v](int i) { return v[i]; };
   auto ys = [](int i) { return y[i]; };
   const double* __restrict__ B = a.B + (size_t)a.mj.jac(k) * a.mj.b_stride;
-  for (int r = 0; r < a.R; ++r) {
+  {
     for (int i = tid; i < c.n; i += kCgThreads) y[i] = B[(size_t)r * a.ldb + a.perm[i]];
     __syncthreads();
     for (int step = 0; step < c.steps; ++step) {   // forward: y_i = fma(-l_ip, y_p, y_i), p ascending
@@ -155,7 +157,7 @@ cudaError_t launch_coopg_factor(const CoopGArgs& a, int K, cudaStream_t stream) 
 
 cudaError_t launch_coopg_solve(const CoopGSolveArgs& a, int K, cudaStream_t stream) {
   if (K <= 0) return cudaSuccess;
-  coopg_solve_kernel<<<K, kCgThreads, coopg_solve_smem(a.c.n), stream>>>(a);
+  coopg_solve_kernel<<<K * a.R, kCgThreads, coopg_solve_smem(a.c.n), stream>>>(a);
   return cudaGetLastError();
 }
 
