@@ -20,7 +20,11 @@ namespace psp {
 
 namespace {
 
-constexpr int kCgThreads = 256;
+#ifndef PSP_CG_THREADS
+#define PSP_CG_THREADS 256
+#endif
+constexpr int kCgThreads = PSP_CG_THREADS;
+constexpr int kCgMinBlocks = 1024 / kCgThreads;   // (64 registers per thread)
 
 __device__ __forceinline__ bool cg_pivot_bad(double piv, double tol) {
   return !(fabs(piv) > tol) || !isfinite(piv);
@@ -65,7 +69,7 @@ __device__ __forceinline__ double cg_chain(double x, const int2* __restrict__ c,
   return x;
 }
 
-__global__ void __launch_bounds__(kCgThreads, 4) coopg_factor_kernel(const __grid_constant__ CoopGArgs a) {
+__global__ void __launch_bounds__(kCgThreads, kCgMinBlocks) coopg_factor_kernel(const __grid_constant__ CoopGArgs a) {
   const CoopGDev& c = a.c;
   __shared__ int st;
   const int k = blockIdx.x, tid = threadIdx.x;
@@ -102,7 +106,7 @@ __global__ void __launch_bounds__(kCgThreads, 4) coopg_factor_kernel(const __gri
   if (tid == 0) a.status[k] = st == INT_MAX ? 0 : st;
 }
 
-__global__ void __launch_bounds__(kCgThreads, 4) coopg_solve_kernel(const __grid_constant__ CoopGSolveArgs a) {
+__global__ void __launch_bounds__(kCgThreads, kCgMinBlocks) coopg_solve_kernel(const __grid_constant__ CoopGSolveArgs a) {
   const CoopGDev& c = a.c;
   extern __shared__ double y[];   // [n]
   // one CTA per (lane, right-hand side): the R solves of a lane run in parallel, sharing
