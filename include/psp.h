@@ -160,6 +160,10 @@ psp_status psp_destroy(psp_handle h);
  *                         factor image lane-major in the handle's factor storage, the same
  *                         etree-level schedule: bitwise the batch kernels); 1: always (when
  *                         built: set before psp_symbolic_analyse); 2: never.  Bitwise-neutral.
+ *  PSP_OPT_FACTOR_HYBRID  (capacity-planned factor) 1: every warp keeps its pending slots
+ *                         0..63 in tensor memory and 64..127 in shared memory (or all 128 in
+ *                         TMEM when alone on its lane quarter) instead of 4 TMEM warps + 3
+ *                         shared-memory warps; 0 (default) / 2: off.  Bitwise-neutral.
  *  PSP_OPT_DATAFLOW       1: psp_factor_solve_batch on a batch that takes the cooperative
  *                         kernels runs ONE fused kernel instead: a CTA per system whose
  *                         factor entries, forward rows and backward rows are dataflow tasks
@@ -197,7 +201,7 @@ enum { PSP_OPT_FACTOR_GROUPS = 1, PSP_OPT_FACTOR_WARPS = 2, PSP_OPT_FACTOR_LANES
        PSP_OPT_FACTOR_SLAB_WARPS = 4, PSP_OPT_FACTOR_PAIRS = 5, PSP_OPT_FACTOR_TMEM = 6,
        PSP_OPT_SOLVE_TMEM = 7, PSP_OPT_PHASE_EVENTS = 8, PSP_OPT_GROWTH = 9,
        PSP_OPT_COOP = 10, PSP_OPT_FACTOR_SPILL = 11, PSP_OPT_PATH = 12, PSP_OPT_COOP_GLOBAL = 13,
-       PSP_OPT_TRANSVERSAL = 14, PSP_OPT_DATAFLOW = 15 };
+       PSP_OPT_TRANSVERSAL = 14, PSP_OPT_DATAFLOW = 15, PSP_OPT_FACTOR_HYBRID = 16 };
 psp_status psp_set_option(psp_handle h, int32_t option, int64_t value);
 
 /* Rebind the handle to another stream of the same device.  Synchronises the old stream

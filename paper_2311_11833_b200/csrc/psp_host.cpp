@@ -138,6 +138,7 @@ struct psp_ctx {
   bool spill_ok = false, spill_aug_ok = false;
   int32_t spill_stats[2][3] = {{0, 0, 0}, {0, 0, 0}};   // [plain, aug] x (spills, reloads, entries)
   int64_t opt_spill = 0;           // PSP_OPT_FACTOR_SPILL: 0 automatic, 1 require, 2 off
+  int64_t opt_hybrid = 0;          // PSP_OPT_FACTOR_HYBRID: 0 automatic, 1 on, 2 off
   DevBuf gspill_d;
   int64_t opt_groups = 0, opt_warps = 0, opt_lanes = 0, opt_slab_warps = 0;  // PSP_OPT_FACTOR_*
   int64_t opt_pairs = 1;                                                      // PSP_OPT_FACTOR_PAIRS
@@ -437,6 +438,10 @@ psp_status psp_set_option(psp_handle h, int32_t option, int64_t value) {
       if (value != 0 && value != 1 && value != 2)
         return fail(h, PSP_ERR_ARG, "PSP_OPT_FACTOR_SLAB_WARPS must be 0, 1 or 2");
       h->opt_slab_warps = value;
+      return PSP_OK;
+    case PSP_OPT_FACTOR_HYBRID:
+      if (value < 0 || value > 2) return fail(h, PSP_ERR_ARG, "PSP_OPT_FACTOR_HYBRID must be 0, 1 or 2");
+      h->opt_hybrid = value;
       return PSP_OK;
     case PSP_OPT_DATAFLOW:
       if (value < 0 || value > 2) return fail(h, PSP_ERR_ARG, "PSP_OPT_DATAFLOW must be 0, 1 or 2");
@@ -910,7 +915,7 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
       Pc.f_npatch = (int32_t)H.f_patch_pos.size();
       Pc.f_gspill = H.f_gspill;
       psp::LaunchInfo lc = h->launch;
-      if (!psp::choose_launch_spill(Pc, lc, (int)h->opt_warps)) continue;
+      if (!psp::choose_launch_spill(Pc, lc, (int)h->opt_warps, h->opt_hybrid == 1)) continue;
       if (!host_only) {
         if ((s = upload(h, H.f_stream, &Pc.f_stream))) return s;
         if ((s = upload(h, H.f_patch_pos, &Pc.f_patch_pos))) return s;

@@ -107,6 +107,7 @@ struct LaunchInfo {
   int f_stages = 4;            // program ring stages of the factor (4 or 8)
   bool f_tmem = false;         // (1, 1, 1) with warps 0..3 holding their slots in TMEM
   bool f_pair_lanes = false;   // compact TMEM kernel, 2 lanes (32-lane slabs) per thread
+  bool f_hybrid = false;       // ... with every warp's slots split TMEM / shared memory (PendHyb)
   int f_off_tscr = 0;          // TMEM warps' scratch rows (shared memory)
   // solve
   bool s_live_smem = false;
@@ -130,7 +131,7 @@ struct LaunchInfo {
 // variant, 2 = disable it.
 bool choose_launch(const DevicePlan& p, LaunchInfo& li, int force_groups, int force_warps,
                    int force_lanes, int force_slab_warps, int force_tmem, int force_solve_tmem);
-bool choose_launch_spill(const DevicePlan& p, LaunchInfo& li, int force_warps);
+bool choose_launch_spill(const DevicePlan& p, LaunchInfo& li, int force_warps, bool hybrid = false);
 cudaError_t configure_kernels(const DevicePlan& p, LaunchInfo& li, int force_groups,
                               int force_warps, int force_lanes, int force_slab_warps,
                               int force_tmem, int force_solve_tmem);
