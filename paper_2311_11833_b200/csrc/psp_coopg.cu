@@ -24,7 +24,10 @@ namespace {
 #define PSP_CG_THREADS 256
 #endif
 constexpr int kCgThreads = PSP_CG_THREADS;
-constexpr int kCgMinBlocks = 1024 / kCgThreads;   // (64 registers per thread)
+#ifndef PSP_CG_MINBLOCKS
+#define PSP_CG_MINBLOCKS (1024 / PSP_CG_THREADS)
+#endif
+constexpr int kCgMinBlocks = PSP_CG_MINBLOCKS;   // (64 registers per thread at 4 x 256)
 
 __device__ __forceinline__ bool cg_pivot_bad(double piv, double tol) {
   return !(fabs(piv) > tol) || !isfinite(piv);
