@@ -163,7 +163,9 @@ psp_status psp_destroy(psp_handle h);
  *  PSP_OPT_FACTOR_HYBRID  (capacity-planned factor) 1: every warp keeps its pending slots
  *                         0..63 in tensor memory and 64..127 in shared memory (or all 128 in
  *                         TMEM when alone on its lane quarter) instead of 4 TMEM warps + 3
- *                         shared-memory warps; 0 (default) / 2: off.  Bitwise-neutral.
+ *                         shared-memory warps; 3: mixed lanes per thread (4 TMEM warps x 64
+ *                         lanes + up to 6 shared-memory warps x 32 lanes); 0 (default) / 2:
+ *                         the default layout (measured fastest).  Bitwise-neutral.
  *  PSP_OPT_DATAFLOW       1: psp_factor_solve_batch on a batch that takes the cooperative
  *                         kernels runs ONE fused kernel instead: a CTA per system whose
  *                         factor entries, forward rows and backward rows are dataflow tasks

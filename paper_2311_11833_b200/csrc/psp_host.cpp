@@ -440,7 +440,7 @@ psp_status psp_set_option(psp_handle h, int32_t option, int64_t value) {
       h->opt_slab_warps = value;
       return PSP_OK;
     case PSP_OPT_FACTOR_HYBRID:
-      if (value < 0 || value > 2) return fail(h, PSP_ERR_ARG, "PSP_OPT_FACTOR_HYBRID must be 0, 1 or 2");
+      if (value < 0 || value > 3) return fail(h, PSP_ERR_ARG, "PSP_OPT_FACTOR_HYBRID must be 0, 1, 2 or 3");
       h->opt_hybrid = value;
       return PSP_OK;
     case PSP_OPT_DATAFLOW:
@@ -915,7 +915,7 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
       Pc.f_npatch = (int32_t)H.f_patch_pos.size();
       Pc.f_gspill = H.f_gspill;
       psp::LaunchInfo lc = h->launch;
-      if (!psp::choose_launch_spill(Pc, lc, (int)h->opt_warps, h->opt_hybrid == 1)) continue;
+      if (!psp::choose_launch_spill(Pc, lc, (int)h->opt_warps, (int)h->opt_hybrid)) continue;
       if (!host_only) {
         if ((s = upload(h, H.f_stream, &Pc.f_stream))) return s;
         if ((s = upload(h, H.f_patch_pos, &Pc.f_patch_pos))) return s;

@@ -108,6 +108,7 @@ struct LaunchInfo {
   bool f_tmem = false;         // (1, 1, 1) with warps 0..3 holding their slots in TMEM
   bool f_pair_lanes = false;   // compact TMEM kernel, 2 lanes (32-lane slabs) per thread
   bool f_hybrid = false;       // ... with every warp's slots split TMEM / shared memory (PendHyb)
+  bool f_mix = false;          // factor_kernel_mix: TMEM warps x 2 lanes, shared-memory warps x 1 lane
   int f_off_tscr = 0;          // TMEM warps' scratch rows (shared memory)
   // solve
   bool s_live_smem = false;
@@ -131,7 +132,8 @@ struct LaunchInfo {
 // variant, 2 = disable it.
 bool choose_launch(const DevicePlan& p, LaunchInfo& li, int force_groups, int force_warps,
                    int force_lanes, int force_slab_warps, int force_tmem, int force_solve_tmem);
-bool choose_launch_spill(const DevicePlan& p, LaunchInfo& li, int force_warps, bool hybrid = false);
+// mode: 0 / 2 default layout, 1 hybrid slot store, 3 mixed lanes per thread
+bool choose_launch_spill(const DevicePlan& p, LaunchInfo& li, int force_warps, int mode = 0);
 cudaError_t configure_kernels(const DevicePlan& p, LaunchInfo& li, int force_groups,
                               int force_warps, int force_lanes, int force_slab_warps,
                               int force_tmem, int force_solve_tmem);

@@ -1,6 +1,7 @@
 """GPU parity of the hybrid slot store of the capacity-planned factor
-(PSP_OPT_FACTOR_HYBRID: every warp keeps slots 0..63 in TMEM and 64..127 in shared memory,
-or all 128 in TMEM when alone on its lane quarter): factors, statuses and solutions
+(PSP_OPT_FACTOR_HYBRID = 1: every warp keeps slots 0..63 in TMEM and 64..127 in shared
+memory, or all 128 in TMEM when alone on its lane quarter; = 3: mixed lanes per thread, 4 TMEM
+warps x 64 lanes + shared-memory warps x 32 lanes): factors, statuses and solutions
 BITWISE those of the default capacity-planned launch (4 TMEM warps + 3 shared-memory
 warps) and of the oracle on sampled lanes; full rounds (7 warps per CTA: partnered and
 lone warps) and partial ones (fewer warps per CTA: all alone), fused and separate."""
@@ -38,13 +39,14 @@ def run(s, eps, hybrid, fused):
     return sv, info, perm, X, st
 
 
+@pytest.mark.parametrize("mode", [1, 3])
 @pytest.mark.parametrize("K,fused", [(1024, True), (20480, False), (65536, True)])
-def test_hybrid_bitwise(K, fused):
+def test_hybrid_bitwise(K, fused, mode):
     s = config(1).system()
     rng = np.random.default_rng(K)
     G = K // 8
     eps = np.concatenate([ladder_eps([e * j for j in range(1, 5)]) for e in 10.0 ** rng.uniform(-3.3, -2.3, G)])
-    sh, info, perm, Xh, sth = run(s, eps, 1, fused)
+    sh, info, perm, Xh, sth = run(s, eps, mode, fused)
     sd, _, _, Xd, std = run(s, eps, 2, fused)
     assert np.array_equal(sth, std) and (sth == 0).all()
     assert np.array_equal(Xh, Xd)
