@@ -189,3 +189,26 @@ def test_dense_D_rejected_on_sparse_path():
     sv.psp_factor_batch(A, 0.0)
     with pytest.raises(psp.PSPError):
         sv.psp_get_factor(0, 10)                  # the sparse layout does not exist
+
+
+def test_dense_many_rhs_and_size_limit():
+    # R = 21 right-hand sides (two 16-column passes, the second ragged) bitwise vs the
+    # oracle; an n beyond the panel's shared memory (N x 33 x 8 B > 227 KB) is refused
+    # with PSP_ERR_UNSUPPORTED, never computed wrongly
+    s = config(0).system()
+    rng = np.random.default_rng(21)
+    B = rng.normal(size=(s.n, 21))
+    eps = np.array([1e-2, -1e-2, 3e-3])
+    tol = oracle.default_tol(s.n, s.row_ptr, s.col_idx, s.vals)
+    g = dense_run(s, eps, tol=tol, B=B)
+    perm = g["perm"]
+    Xo, sto = oracle.dense_batch(s, perm, eps, tol, B=B)
+    assert (sto == 0).all() and np.array_equal(g["X"], Xo)
+    big = config(3).system()               # n = 3600 -> N = 3616: 954 KB panel
+    sv = psp.Solver(0)
+    sv.psp_set_option("path", "dense")
+    sv.psp_symbolic_analyse(big.n, big.row_ptr, big.col_idx)
+    sv.psp_set_perturbations(np.array([1e-3]), big.d)
+    with pytest.raises(psp.PSPError) as e:
+        sv.psp_factor_batch(torch.tensor(big.vals, dtype=torch.float64, device="cuda"), 0.0)
+    assert e.value.status == 8
