@@ -12,9 +12,10 @@
 // dense_lu_kernel: one CTA (8 warps) per lane, right-looking blocked elimination in
 // panels of 32 columns:
 //   1. perturb (Alg. 1 step 1, fused): the CTA writes M_k row by row;
-//   2. per panel kb: the (N-kb) x 32 panel in shared memory, unblocked elimination
-//      (l = a / u_pp, then fma(-l, u_pj, a_ij), ascending p) with the status check of
-//      R10 on every pivot;
+//   2. per panel kb: the (N-kb) x 32 panel in shared memory; its 32 x 32 diagonal block
+//      eliminated by one warp in registers (l = a / u_pp, then fma(-l, u_pj, a_ij),
+//      ascending p; the status check of R10 on every pivot), then the rows below it
+//      row by row (each entry's updates in ascending p, then its division);
 //   3. U12 = L11^{-1} A12, one column per thread in registers (ascending p);
 //   4. A22 -= L21 U12 on the tensor path: 32 x 32 tiles per warp, C in registers
 //      (16 DMMA fragments), L21 (negated) from the shared-memory panel, U12 from L1/L2,
@@ -78,6 +79,24 @@ __device__ __noinline__ void trsm_column(double* __restrict__ col, int N, const 
   for (int i = 1; i < kDNB; ++i) col[(size_t)i * N] = u[i];
 }
 
+// A panel row below the diagonal block: pr[j] <- (pr[j] - sum_{q<j} l_q u_qj, q ascending) /
+// u_jj with l_q the row's own new values and u from the factored diagonal block (u_qj at
+// ps[q * kDPS + j]).
+__device__ __noinline__ void panel_row(double* __restrict__ pr, const double* ps) {
+  double a[kDNB];
+#pragma unroll
+  for (int j = 0; j < kDNB; ++j) a[j] = pr[j];
+#pragma unroll
+  for (int j = 0; j < kDNB; ++j) {
+    asm volatile("" ::: "memory");   // keep column j's U loads next to their use
+#pragma unroll
+    for (int q = 0; q < j; ++q) a[j] = __fma_rn(-a[q], ps[q * kDPS + j], a[j]);
+    a[j] = a[j] / ps[j * kDPS + j];
+  }
+#pragma unroll
+  for (int j = 0; j < kDNB; ++j) pr[j] = a[j];
+}
+
 template <bool kDenseD>
 __global__ void __launch_bounds__(kDThreads, 1) dense_lu_kernel(const __grid_constant__ DenseArgs a) {
   extern __shared__ double ps[];   // panel: (N - kb) rows x kDPS
@@ -125,17 +144,40 @@ __global__ void __launch_bounds__(kDThreads, 1) dense_lu_kernel(const __grid_con
     // 2. panel rows kb..N-1, columns kb..kb+31
     for (int r = warp; r < M; r += kDWarps) ps[r * kDPS + lane] = Mk[(size_t)(kb + r) * N + kb + lane];
     __syncthreads();
-    for (int p = 0; p < kDNB; ++p) {
-      const double piv = ps[p * kDPS + p];
-      if (tid == 0 && st == 0 && kb + p < n && dense_pivot_bad(piv, tol)) st = kb + p + 1;
-      for (int r = p + 1 + tid; r < M; r += kDThreads) {
-        double* pr = ps + r * kDPS;
-        const double l = pr[p] / piv;
-        pr[p] = l;
-        for (int j = p + 1; j < kDNB; ++j) pr[j] = __fma_rn(-l, ps[p * kDPS + j], pr[j]);
+    // 2a. the 32 x 32 diagonal block by warp 0, lane r = panel row r in registers, right-
+    //     looking: at step p lane p publishes its (final) U row, the lanes below divide
+    //     (in parallel) and update their row -- entry (r, j) gets pivot p's update at step p
+    if (warp == 0) {
+      double row[kDNB];
+#pragma unroll
+      for (int j = 0; j < kDNB; ++j) row[j] = ps[lane * kDPS + j];
+#pragma unroll
+      for (int p = 0; p < kDNB; ++p) {
+        if (lane == p) {
+#pragma unroll
+          for (int j = p; j < kDNB; ++j) ps[p * kDPS + j] = row[j];
+        }
+        __syncwarp();
+        const double piv = ps[p * kDPS + p];
+        if (lane == 0 && st == 0 && kb + p < n && dense_pivot_bad(piv, tol)) st = kb + p + 1;
+        if (lane > p) {
+          const double l = row[p] / piv;
+          row[p] = l;
+#pragma unroll
+          for (int j = p + 1; j < kDNB; ++j) row[j] = __fma_rn(-l, ps[p * kDPS + j], row[j]);
+        }
+        __syncwarp();
       }
-      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < kDNB; ++j)
+        if (j < lane) ps[lane * kDPS + j] = row[j];
     }
+    __syncthreads();
+    // 2b. the panel's rows below it, one row per thread, row-oriented: entry (r, j) gets
+    //     the updates of pivots q = 0 .. j-1 in ascending order, then l_rj = a_rj / u_jj --
+    //     the same per-entry sequence as the right-looking steps, without 32 CTA barriers
+    for (int r = kDNB + tid; r < M; r += kDThreads) panel_row(ps + r * kDPS, ps);
+    __syncthreads();
     for (int r = warp; r < M; r += kDWarps) Mk[(size_t)(kb + r) * N + kb + lane] = ps[r * kDPS + lane];
     if (M == kDNB) break;
     // 3. U12 = L11^{-1} A12: rows kb..kb+31, one column per thread
