@@ -1,6 +1,6 @@
 """Instructions executed and stall samples of one kernel per CUDA source line.
 
-usage: python tools/ncu_lines.py REPORT.ncu-rep CUBIN KERNEL_SUBSTRING [top]
+usage: python tools/ncu_lines.py REPORT.ncu-rep CUBIN KERNEL_SUBSTRING [top [SRCDIR]]
 Maps ncu's SASS rows (by offset from the kernel's first instruction) to source lines
 with `nvdisasm -g` (build with -lineinfo)."""
 import csv
@@ -18,9 +18,9 @@ def line_map(cubin, kernel):
         if f:
             cur_fn = f.group(1)
             continue
-        g = re.search(r'//## File ".*?", line (\d+)', ln)
+        g = re.search(r'//## File "(.*?)", line (\d+)', ln)
         if g:
-            line = int(g.group(1))
+            line = (g.group(1).split("/")[-1], int(g.group(2)))
             continue
         a = re.match(r"\s*/\*([0-9a-f]{4,})\*/", ln)
         if a and cur_fn and kernel in cur_fn:
@@ -46,10 +46,23 @@ def main():
         ex[ln] += num(r[iE])
         st[ln] += num(r[iS])
     tE, tS = sum(ex.values()), sum(st.values())
-    src = open(sys.argv[5]).read().splitlines() if len(sys.argv) > 5 else None
+    srcdir = sys.argv[5] if len(sys.argv) > 5 else None
+    cache = {}
+
+    def text(ln):
+        if not (srcdir and ln):
+            return ""
+        f, n = ln
+        if f not in cache:
+            try:
+                cache[f] = open(f"{srcdir}/{f}").read().splitlines()
+            except OSError:
+                cache[f] = []
+        return cache[f][n - 1].strip()[:70] if n <= len(cache[f]) else ""
+
     for ln in sorted(ex, key=lambda k: -st[k])[:top]:
-        s = src[ln - 1].strip()[:70] if src and ln else ""
-        print(f"line {ln!s:>5} exec {ex[ln] / tE:6.1%} stall {st[ln] / tS:6.1%}  {s}")
+        name = f"{ln[0]}:{ln[1]}" if ln else "?"
+        print(f"{name:>24} exec {ex[ln] / tE:6.1%} stall {st[ln] / tS:6.1%}  {text(ln)}")
 
 
 if __name__ == "__main__":
