@@ -894,6 +894,7 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
   //          + nbd diagonal births  [slot, 0, a_ii (2), d_i (2), 0, 0]: a_ii + eps*d_i
   //          + nba births           [slot, 0, a_ij (2)] (structural zeros: a_ij = 0);
   //            nba is a multiple of 4 (padding births write a dummy slot never read)
+  //            (all-slot programs: births in groups of 4, see put_births)
   //          + c L operands, cu U operands (4 words each; cu = c (+ 1: y_p of [A | b]),
   //            padded to a multiple of 4 with immediate zeros)
   //          + (flags & 2 == 0) c rows x ws target slots of the c x c update block
@@ -964,6 +965,46 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
     }
     ++P.f_births;
   };
+  // Births of d[d0, d1) (diagonal entries) and o[o0, o1) (the others) appended to record r;
+  // returns the record's (nbd, nba) counts.  Plain programs: per birth [slot, 0, a (2)
+  // (, d_i (2), 0, 0)], nba padded to 4.  All-slot programs (the capacity-planned kernel):
+  // groups of 4, [4 slots] + 4 x [a_ii, d_i] (20 words) or 4 x [a] (12 words), both
+  // counts padded to 4 (the dummy slot): 5 + 3 instead of 8 + 4 words per birth (the
+  // program ring's chunks go further; its waits are a measured cost of this kernel).
+  auto ceil4 = [](size_t k) { return (k + 3) & ~(size_t)3; };
+  auto birth_words = [&](size_t nd, size_t no) {
+    return P.all_slots ? 5 * ceil4(nd) + 3 * ceil4(no) : 8 * nd + 4 * ceil4(no);
+  };
+  auto put_births = [&](std::vector<int32_t>& r, std::vector<std::pair<int32_t, int32_t>>& pt,
+                        const std::vector<int32_t>& d, size_t d0, size_t d1, const std::vector<int32_t>& o,
+                        size_t o0, size_t o1) -> std::pair<int32_t, int32_t> {
+    if (!P.all_slots) {
+      for (size_t k = d0; k < d1; ++k) birth(r, pt, d[k]);
+      for (size_t k = o0; k < o1; ++k) birth(r, pt, o[k]);
+      for (size_t k = o1 - o0; k < ceil4(o1 - o0); ++k) r.insert(r.end(), {dummy_slot, 0, 0, 0});
+      return {(int32_t)(d1 - d0), (int32_t)ceil4(o1 - o0)};
+    }
+    auto groups = [&](const std::vector<int32_t>& v, size_t b0, size_t b1, bool diag) {
+      for (size_t g = b0; g < b1; g += 4) {
+        for (size_t k = g; k < g + 4; ++k) r.push_back(k < b1 ? slot_of(v[k]) : dummy_slot);
+        for (size_t k = g; k < g + 4; ++k) {
+          if (k >= b1) {
+            r.insert(r.end(), {0, 0});
+            if (diag) r.insert(r.end(), {0, 0});
+            continue;
+          }
+          const int32_t e = v[k], i = ent_i[e], j = ent_j[e];
+          sim_slot[slot_of(e)] = e;
+          imm(r, pt, a_src(i, j));
+          if (diag) imm(r, pt, -1 - i);
+          ++P.f_births;
+        }
+      }
+    };
+    groups(d, d0, d1, true);
+    groups(o, o0, o1, false);
+    return {(int32_t)ceil4(d1 - d0), (int32_t)ceil4(o1 - o0)};
+  };
   P.adiag.assign(n, -1);
   for (int32_t i = 0; i < n; ++i) P.adiag[i] = a_index(i, i);
   // SPILL / RELOAD  [type<<28 | cnt, 0, 0, 0] + cnt x [slot, gidx] (cnt a multiple of 4:
@@ -992,16 +1033,18 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
   // pivot's, emitted after its PIVOT record)
   auto birth_records = [&](const std::vector<int32_t>& bd, const std::vector<int32_t>& bo, size_t& qd,
                            size_t& qo, size_t budget) {
-    while (budget + 8 * (bd.size() - qd) + 4 * (bo.size() - qo) > kMaxRec &&
+    while (budget + birth_words(bd.size() - qd, bo.size() - qo) > kMaxRec &&
            (qd < bd.size() || qo < bo.size())) {
       std::vector<int32_t> b = {(int32_t)(kRecBirth << 28), 0, 0, 0, 0, 0, 0, 0};
       std::vector<std::pair<int32_t, int32_t>> pt;
-      int32_t nd = 0, no = 0;
-      while (qd < bd.size() && b.size() + 8 <= kMaxRec) birth(b, pt, bd[qd++]), ++nd;
-      while (qo < bo.size() && b.size() + 4 <= kMaxRec - 12) birth(b, pt, bo[qo++]), ++no;
-      while (no % 4) b.insert(b.end(), {dummy_slot, 0, 0, 0}), ++no;
-      b[2] = nd;
-      b[3] = no;
+      size_t nd = 0, no = 0;   // as many as fit one record: diagonal ones first
+      while (qd + nd < bd.size() && 8 + birth_words(nd + 1, 0) <= kMaxRec) ++nd;
+      while (qo + no < bo.size() && 8 + birth_words(nd, no + 1) <= kMaxRec) ++no;
+      const auto cnt = put_births(b, pt, bd, qd, qd + nd, bo, qo, qo + no);
+      qd += nd;
+      qo += no;
+      b[2] = cnt.first;
+      b[3] = cnt.second;
       push(std::move(b), std::move(pt));
     }
   };
@@ -1035,15 +1078,17 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
     birth_records(bd, bo, qd, qo, fixed);   // births that do not fit the record go first
     const int32_t e_pp = entry(p, p);
     const int32_t flags = (first[e_pp] < 0 ? 1 : 0) | (fused ? 0 : 2) | (paired[p] ? 4 : 0);
-    const int32_t nbo = (int32_t)(bo.size() - qo), nbo4 = (nbo + 3) & ~3;
-    std::vector<int32_t> r = {(int32_t)((kRecPivot << 28) | (uint32_t)c), p,
-                              (int32_t)(bd.size() - qd), nbo4, flags, ws};
+    std::vector<int32_t> r = {(int32_t)((kRecPivot << 28) | (uint32_t)c), p, 0, 0, flags, ws};
     std::vector<std::pair<int32_t, int32_t>> pt;
     imm(r, pt, -1 - p);
     operand(r, pt, p, p);
-    while (qd < bd.size()) birth(r, pt, bd[qd++]);
-    while (qo < bo.size()) birth(r, pt, bo[qo++]);
-    for (int32_t k = nbo; k < nbo4; ++k) r.insert(r.end(), {dummy_slot, 0, 0, 0});
+    {
+      const auto cnt = put_births(r, pt, bd, qd, bd.size(), bo, qo, bo.size());
+      qd = bd.size();
+      qo = bo.size();
+      r[2] = cnt.first;
+      r[3] = cnt.second;
+    }
     for (int32_t k = 0; k < c; ++k) operand(r, pt, L[k], p);
     for (int32_t k = 0; k < c; ++k) operand(r, pt, p, L[k]);
     if (aug) operand(r, pt, p, n);   // y_p
@@ -1092,12 +1137,11 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
           if (zd < cd.size() || zo < co.size()) {   // the rest (fits one record)
             std::vector<int32_t> b = {(int32_t)(kRecBirth << 28), 0, 0, 0, 0, 0, 0, 0};
             std::vector<std::pair<int32_t, int32_t>> pt2;
-            int32_t nd = 0, no = 0;
-            while (zd < cd.size()) birth(b, pt2, cd[zd++]), ++nd;
-            while (zo < co.size()) birth(b, pt2, co[zo++]), ++no;
-            while (no % 4) b.insert(b.end(), {dummy_slot, 0, 0, 0}), ++no;
-            b[2] = nd;
-            b[3] = no;
+            const auto cnt = put_births(b, pt2, cd, zd, cd.size(), co, zo, co.size());
+            zd = cd.size();
+            zo = co.size();
+            b[2] = cnt.first;
+            b[3] = cnt.second;
             push(std::move(b), std::move(pt2));
           }
           updates(r0, r1);
