@@ -129,6 +129,13 @@ psp_status psp_destroy(psp_handle h);
  *                         slab (G = J = 1 only), the rows of each pivot split between them.
  *  PSP_OPT_FACTOR_PAIRS   1 (default): fuse supernode pivot pairs (p, p+1 with
  *                         L(:,p) = {p+1} u L(:,p+1)) into one record; 0: off.
+ *  PSP_OPT_SKIP_ZERO_ROWS 1 (default): the symbolic analysis marks the multipliers l_{i p} that
+ *                         are structural zeros of A's own (unsymmetric) pattern inside the fill of
+ *                         the symmetrised pattern, and the capacity-planned batch factor stores
+ *                         l = 0 for them instead of the division and the row update
+ *                         fma(-0, u, x) = x (the identity the sparse code already relies on for
+ *                         entries outside the fill); 0: every row of the fill is computed.
+ *                         Takes effect at the next psp_symbolic_analyse.
  *  PSP_OPT_FACTOR_WARPS   0 (default): automatic; else consumer warps per factor CTA
  *                         (1..16, capped by shared memory).
  *  PSP_OPT_FACTOR_TMEM    0 (default): automatic; 1: require, 2: disable the factor
@@ -203,7 +210,8 @@ enum { PSP_OPT_FACTOR_GROUPS = 1, PSP_OPT_FACTOR_WARPS = 2, PSP_OPT_FACTOR_LANES
        PSP_OPT_FACTOR_SLAB_WARPS = 4, PSP_OPT_FACTOR_PAIRS = 5, PSP_OPT_FACTOR_TMEM = 6,
        PSP_OPT_SOLVE_TMEM = 7, PSP_OPT_PHASE_EVENTS = 8, PSP_OPT_GROWTH = 9,
        PSP_OPT_COOP = 10, PSP_OPT_FACTOR_SPILL = 11, PSP_OPT_PATH = 12, PSP_OPT_COOP_GLOBAL = 13,
-       PSP_OPT_TRANSVERSAL = 14, PSP_OPT_DATAFLOW = 15, PSP_OPT_FACTOR_HYBRID = 16 };
+       PSP_OPT_TRANSVERSAL = 14, PSP_OPT_DATAFLOW = 15, PSP_OPT_FACTOR_HYBRID = 16,
+       PSP_OPT_SKIP_ZERO_ROWS = 17 };
 psp_status psp_set_option(psp_handle h, int32_t option, int64_t value);
 
 /* Rebind the handle to another stream of the same device.  Synchronises the old stream

@@ -141,6 +141,7 @@ struct psp_ctx {
   int64_t opt_hybrid = 0;          // PSP_OPT_FACTOR_HYBRID: 0 automatic, 1 on, 2 off
   DevBuf gspill_d;
   int64_t opt_groups = 0, opt_warps = 0, opt_lanes = 0, opt_slab_warps = 0;  // PSP_OPT_FACTOR_*
+  int64_t opt_skip_dead = 1;                                                  // PSP_OPT_SKIP_ZERO_ROWS
   int64_t opt_pairs = 1;                                                      // PSP_OPT_FACTOR_PAIRS
   int64_t opt_tmem = 0;                                                       // PSP_OPT_FACTOR_TMEM
   int64_t opt_solve_tmem = 0;                                                 // PSP_OPT_SOLVE_TMEM
@@ -434,6 +435,10 @@ psp_status psp_set_option(psp_handle h, int32_t option, int64_t value) {
       if (value != 0 && value != 1) return fail(h, PSP_ERR_ARG, "PSP_OPT_FACTOR_PAIRS must be 0 or 1");
       h->opt_pairs = value;
       return PSP_OK;
+    case PSP_OPT_SKIP_ZERO_ROWS:
+      if (value != 0 && value != 1) return fail(h, PSP_ERR_ARG, "PSP_OPT_SKIP_ZERO_ROWS must be 0 or 1");
+      h->opt_skip_dead = value;
+      return PSP_OK;
     case PSP_OPT_FACTOR_SLAB_WARPS:
       if (value != 0 && value != 1 && value != 2)
         return fail(h, PSP_ERR_ARG, "PSP_OPT_FACTOR_SLAB_WARPS must be 0, 1 or 2");
@@ -654,6 +659,7 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
 
   psp::HostPlan HP, HPa;
   HP.fuse_pairs = HPa.fuse_pairs = h->opt_pairs != 0;
+  HP.skip_dead = HPa.skip_dead = h->opt_skip_dead != 0;
   HPa.aug = true;
   psp::build_programs(n, S.lcol, perm, row_ptr_h, col_idx_h, HP);
   psp::build_programs(n, S.lcol, perm, row_ptr_h, col_idx_h, HPa);
@@ -662,6 +668,7 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
   // capacity-planned programs (spills) for the 2-CTA TMEM factor kernel
   psp::HostPlan HPc, HPac;
   HPc.fuse_pairs = HPac.fuse_pairs = h->opt_pairs != 0;
+  HPc.skip_dead = HPac.skip_dead = h->opt_skip_dead != 0;
   HPac.aug = true;
   HPc.cap = HPac.cap = kSpillCap;
   HPc.all_slots = HPac.all_slots = true;

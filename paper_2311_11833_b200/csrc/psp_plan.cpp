@@ -28,6 +28,7 @@
 #include <climits>
 #include <cstdint>
 #include <functional>
+#include <cstdio>
 #include <cstdlib>
 #include <set>
 
@@ -663,6 +664,27 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
   std::vector<std::vector<int32_t>> births_at(n);
   for (int32_t e = 0; e < n_ent; ++e)
     if (first[e] >= 0) births_at[first[e]].push_back(e);
+  // Structural liveness under A's own pattern.  The fill above is that of the symmetrised
+  // pattern A + A^T (one elimination tree for rows and columns); an entry of it that is
+  // absent from A and receives no update l_{i k} u_{k j} with both factors structurally
+  // non-zero is exactly +0 in every lane when it is consumed.  For such an L operand
+  // a_{i p} the multiplier is l_{i p} = 0 and its whole row update fma(-0, u, x) = x is
+  // the identity (as for the entries outside the fill, which no sparse code touches):
+  // the row is dead: the capacity-planned fused records list it after the live rows,
+  // without its tile row, and the batch factor only stores l = 0.
+  std::vector<char> live(n_ent, 1);
+  if (P.skip_dead) {
+    for (int32_t e = n; e < n + 2 * (int32_t)nnzL; ++e) live[e] = a_index(ent_i[e], ent_j[e]) >= 0;
+    for (int32_t p = 0; p < n; ++p) {
+      const auto& L = lcol[p];
+      for (size_t a = 0; a < L.size(); ++a) {
+        if (!live[n + off[p] + a]) continue;            // L(L[a], p)
+        for (size_t b = 0; b < L.size(); ++b)
+          if (live[n + nnzL + off[p] + b]) live[entry(L[a], L[b])] = 1;   // U(p, L[b])
+      }
+    }
+  }
+  P.f_dead_rows = 0;
   // Slot-store capacity (HostPlan::cap): the peak pending set of the unlimited plan
   // (interval colouring) decides whether the capacity-planned program is needed.
   std::vector<int32_t> fslot;
@@ -901,6 +923,9 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
   //          flags: 1 = the pivot was never updated (add eps*d_p); 2 = c > kFusedMax,
   //          the update comes in UPDATE records; 4 = supernode pair: the record also
   //          carries pivot q = p + 1 (row 0 of the block is q's row, column 0 its column);
+  //          bits 8..15 = number of dead rows (l_{i p} a structural zero, below): listed
+  //          last among the L operands, without tile rows; L operand word 1 = the row's
+  //          position in the stored L column;
   //          ws = row stride (8 * ceil(cu / 8)); padding columns hold the dummy slot
   //   BIRTH  [1<<28, 0, nbd, nba, 0, 0, 0, 0] + births: those of the next pivot that do
   //          not fit its record
@@ -1089,7 +1114,28 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
       r[2] = cnt.first;
       r[3] = cnt.second;
     }
-    for (int32_t k = 0; k < c; ++k) operand(r, pt, L[k], p);
+    // Row order of the record: the stored order (ascending rows), or -- capacity-planned
+    // fused records -- the live rows first and the dead rows (see `live` above; a pair's
+    // row also needs a dead a_{i q}, and row 0 of a pair, q's own row, stays first) last,
+    // without tile rows.  Operand word 1 = the row's position in the stored L column.
+    std::vector<int32_t> rord;
+    int32_t n_dead = 0;
+    {
+      std::vector<int32_t> deadr;
+      for (int32_t k = 0; k < c; ++k) {
+        const bool dead = P.skip_dead && P.all_slots && fused && !live[entry(L[k], p)] &&
+                          (!paired[p] || (k > 0 && !live[entry(L[k], p + 1)]));
+        (dead ? deadr : rord).push_back(k);
+      }
+      n_dead = (int32_t)deadr.size();
+      rord.insert(rord.end(), deadr.begin(), deadr.end());
+      P.f_dead_rows += n_dead;
+      r[4] |= n_dead << 8;   // flags bits 8..15: dead rows
+    }
+    for (int32_t k : rord) {
+      operand(r, pt, L[k], p);
+      r[r.size() - 3] = k;
+    }
     for (int32_t k = 0; k < c; ++k) operand(r, pt, p, L[k]);
     if (aug) operand(r, pt, p, n);   // y_p
     for (int32_t k = cu; k < cu4; ++k)   // (all_slots: the dummy slot, else an immediate 0)
@@ -1105,7 +1151,7 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
         }
     };
     if (fused)
-      for (int32_t a = 0; a < c; ++a) row(r, a);
+      for (int32_t a = 0; a < c - n_dead; ++a) row(r, rord[a]);
     push(std::move(r), std::move(pt));
     if (paired[p]) ++p;   // q's work is in p's record
     if (!fused) {
@@ -1154,6 +1200,12 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
   push({(int32_t)(kRecEnd << 28), 0, 0, 0}, {});
   pack_chunks(recs, max_rec, P.f_chunk_words, P.f_stream, &rec_patch, &P.f_patch_pos,
               &P.f_patch_src);
+  if (std::getenv("PSP_DEBUG_PLAN")) {
+    int64_t dead_l = 0;
+    for (int32_t e = n; e < n + (int32_t)nnzL; ++e) dead_l += !live[e];
+    std::fprintf(stderr, "[psp plan] aug=%d capped=%d nnz_L=%lld dead L entries=%lld rows marked=%d pairs=%d words=%zu\n",
+                 (int)aug, (int)capped, (long long)nnzL, (long long)dead_l, P.f_dead_rows, P.f_pairs, P.f_stream.size());
+  }
 
   // ---------------- solve program ----------------
   // Forward substitution (column-oriented, pivots ascending):

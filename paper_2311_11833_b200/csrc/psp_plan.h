@@ -24,6 +24,10 @@ struct HostPlan {
   // record streams packed in chunks
   int32_t f_slots = 0, f_births = 0, f_chunk_words = 0, f_pairs = 0;
   bool fuse_pairs = true;          // input: fuse supernode pivot pairs into one record
+  // input: mark the L operands that are structural zeros of A's own (unsymmetric) pattern
+  // inside the symmetrised fill (listed last in a fused record): the batch factor skips their rows
+  bool skip_dead = true;
+  int32_t f_dead_rows = 0;         // rows marked (of nnz_L)
   // input: factor program of the AUGMENTED matrix [A | b] (column n = one right-hand
   // side, never a pivot): every U row gets u_{p b} = y_p, the forward-substitution
   // result, which the factor kernel writes to X instead of the DU region

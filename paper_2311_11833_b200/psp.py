@@ -37,7 +37,7 @@ PATH = {"sparse": 0, "dense": 1}
 OPT = {"factor_groups": 1, "factor_warps": 2, "factor_lanes": 3, "factor_slab_warps": 4,
        "factor_pairs": 5, "factor_tmem": 6, "solve_tmem": 7, "phase_events": 8, "growth": 9, "coop": 10,
        "factor_spill": 11, "path": 12, "coop_global": 13,
-       "transversal": 14, "dataflow": 15, "factor_hybrid": 16}
+       "transversal": 14, "dataflow": 15, "factor_hybrid": 16, "skip_zero_rows": 17}
 
 
 class SymbolicInfo(ctypes.Structure):
