@@ -105,6 +105,10 @@ typedef struct {
    * (plain program; aug_spill_ops for [A | b]); spill_entries = spill-area entries per lane;
    * spill_warps_per_cta = warps of the 2-CTA-per-SM launch */
   int32_t spill_ok, spill_cap, spill_ops, spill_entries, aug_spill_ops, spill_warps_per_cta;
+  /* PSP_OPT_SKIP_ZERO_ROWS: struct_zero_l = multipliers l_{i p} of the (symmetrised) fill that
+   * are structural zeros of A's own pattern (0 with the option off); skipped_rows /
+   * aug_skipped_rows = rows the capacity-planned programs (plain / [A | b]) skip */
+  int32_t struct_zero_l, skipped_rows, aug_skipped_rows;
 } psp_symbolic_info;
 
 /* ---- lifetime ---------------------------------------------------------------- */

@@ -101,6 +101,35 @@ def filled_pattern(n, row_ptr, col_idx, perm):
     return colptr, np.array(rows, dtype=np.int32)
 
 
+def unsymmetric_structure(n, row_ptr, col_idx, perm):
+    """Structure of L + U for the pivot-free elimination of P A P^T under A's OWN pattern
+    (no symmetrisation): the plain definition -- entry (i, j) is structurally non-zero if
+    it is on the diagonal (a_ii + eps d_i), in pattern(A), or receives an update
+    l_{i p} u_{p j} with both factors structurally non-zero, pivots p ascending.  Returns
+    the list of row sets (permuted numbering).  Every entry of filled_pattern() that is not
+    in this structure is exactly 0 in every lane of the dense pivot-free factorisation
+    (pinned numerically in tests/test_oracle_structure.py)."""
+    inv = np.empty(n, dtype=np.int64)
+    inv[np.asarray(perm)] = np.arange(n)
+    rows = [set([i]) for i in range(n)]
+    for i in range(n):
+        for q in range(row_ptr[i], row_ptr[i + 1]):
+            rows[int(inv[i])].add(int(inv[col_idx[q]]))
+    cols = [set() for _ in range(n)]
+    for i in range(n):
+        for j in rows[i]:
+            cols[j].add(i)
+    for p in range(n):
+        lp = [i for i in cols[p] if i > p]
+        up = [j for j in rows[p] if j > p]
+        for i in lp:
+            for j in up:
+                if j not in rows[i]:
+                    rows[i].add(j)
+                    cols[j].add(i)
+    return rows
+
+
 def permuted_csc(n, row_ptr, col_idx, vals, perm):
     """CSC of P A P^T (values copied, no arithmetic)."""
     inv = np.empty(n, dtype=np.int64)

@@ -136,6 +136,7 @@ struct psp_ctx {
   DevicePlan plan_spill, plan_spill_aug;
   psp::LaunchInfo launch_spill, launch_spill_aug;
   bool spill_ok = false, spill_aug_ok = false;
+  int32_t dead_l = 0, dead_rows[2] = {0, 0};   // structural-zero multipliers; rows skipped [plain, aug]
   int32_t spill_stats[2][3] = {{0, 0, 0}, {0, 0, 0}};   // [plain, aug] x (spills, reloads, entries)
   int64_t opt_spill = 0;           // PSP_OPT_FACTOR_SPILL: 0 automatic, 1 require, 2 off
   int64_t opt_hybrid = 0;          // PSP_OPT_FACTOR_HYBRID: 0 automatic, 1 on, 2 off
@@ -910,6 +911,8 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
   // capacity-planned variants (same V layout as the (1, 1, 1) launches: 32-lane slabs)
   h->spill_ok = h->spill_aug_ok = false;
   std::memset(h->spill_stats, 0, sizeof h->spill_stats);
+  h->dead_l = HP.f_dead_l;
+  h->dead_rows[0] = h->dead_rows[1] = 0;
   if (try_spill && h->launch.f_groups == 1 && h->launch.f_lanes == 1 && h->launch.f_slab_warps == 1) {
     for (int q = 0; q < 2; ++q) {
       const psp::HostPlan& H = q ? HPac : HPc;
@@ -934,6 +937,7 @@ psp_status psp_symbolic_analyse(psp_handle h, int32_t n, const int32_t* row_ptr_
       h->spill_stats[q][0] = H.f_spills;
       h->spill_stats[q][1] = H.f_reloads;
       h->spill_stats[q][2] = H.f_gspill;
+      h->dead_rows[q] = H.f_dead_rows;
     }
   }
   if (h->opt_spill == 1 && !h->spill_ok)
@@ -1022,6 +1026,9 @@ psp_status psp_get_symbolic_info(psp_handle h, psp_symbolic_info* info, int32_t*
   info->spill_entries = h->spill_stats[0][2];
   info->aug_spill_ops = h->spill_stats[1][0] + h->spill_stats[1][1];
   info->spill_warps_per_cta = h->spill_ok ? h->launch_spill.f_warps : 0;
+  info->struct_zero_l = h->dead_l;
+  info->skipped_rows = h->dead_rows[0];
+  info->aug_skipped_rows = h->dead_rows[1];
   if (perm_h) std::copy(h->perm.begin(), h->perm.end(), perm_h);
   return PSP_OK;
 }

@@ -685,6 +685,8 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
     }
   }
   P.f_dead_rows = 0;
+  P.f_dead_l = 0;
+  for (int32_t e = n; e < n + (int32_t)nnzL; ++e) P.f_dead_l += !live[e];
   // Slot-store capacity (HostPlan::cap): the peak pending set of the unlimited plan
   // (interval colouring) decides whether the capacity-planned program is needed.
   std::vector<int32_t> fslot;
@@ -1200,12 +1202,6 @@ void build_programs(int32_t n, const std::vector<std::vector<int32_t>>& lcol,
   push({(int32_t)(kRecEnd << 28), 0, 0, 0}, {});
   pack_chunks(recs, max_rec, P.f_chunk_words, P.f_stream, &rec_patch, &P.f_patch_pos,
               &P.f_patch_src);
-  if (std::getenv("PSP_DEBUG_PLAN")) {
-    int64_t dead_l = 0;
-    for (int32_t e = n; e < n + (int32_t)nnzL; ++e) dead_l += !live[e];
-    std::fprintf(stderr, "[psp plan] aug=%d capped=%d nnz_L=%lld dead L entries=%lld rows marked=%d pairs=%d words=%zu\n",
-                 (int)aug, (int)capped, (long long)nnzL, (long long)dead_l, P.f_dead_rows, P.f_pairs, P.f_stream.size());
-  }
 
   // ---------------- solve program ----------------
   // Forward substitution (column-oriented, pivots ascending):

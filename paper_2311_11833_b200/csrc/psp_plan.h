@@ -27,7 +27,8 @@ struct HostPlan {
   // input: mark the L operands that are structural zeros of A's own (unsymmetric) pattern
   // inside the symmetrised fill (listed last in a fused record): the batch factor skips their rows
   bool skip_dead = true;
-  int32_t f_dead_rows = 0;         // rows marked (of nnz_L)
+  int32_t f_dead_rows = 0;         // rows skipped by the program (of nnz_L)
+  int32_t f_dead_l = 0;            // structural-zero multipliers found (with skip_dead)
   // input: factor program of the AUGMENTED matrix [A | b] (column n = one right-hand
   // side, never a pivot): every U row gets u_{p b} = y_p, the forward-substitution
   // result, which the factor kernel writes to X instead of the DU region

@@ -54,7 +54,8 @@ class SymbolicInfo(ctypes.Structure):
                 ("aug_pend_smem", ctypes.c_int32), ("spill_ok", ctypes.c_int32),
                 ("spill_cap", ctypes.c_int32), ("spill_ops", ctypes.c_int32),
                 ("spill_entries", ctypes.c_int32), ("aug_spill_ops", ctypes.c_int32),
-                ("spill_warps_per_cta", ctypes.c_int32)]
+                ("spill_warps_per_cta", ctypes.c_int32), ("struct_zero_l", ctypes.c_int32),
+                ("skipped_rows", ctypes.c_int32), ("aug_skipped_rows", ctypes.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
