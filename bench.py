@@ -106,8 +106,27 @@ def config_points(psp, torch, stream, device):
     return res
 
 
+_JSON_FD = None
+
+
+def _stdout_json_only():
+    """Keep the process's stdout for the JSON line alone: file descriptor 1 is pointed at
+    stderr for everything else (NCCL prints its version banner to stdout from C)."""
+    global _JSON_FD
+    if _JSON_FD is None:
+        sys.stdout.flush()
+        _JSON_FD = os.dup(1)
+        os.dup2(2, 1)
+
+
 def _json_print(d):
-    print(json.dumps(d), flush=True)
+    line = json.dumps(d) + "\n"
+    if _JSON_FD is None:
+        sys.stdout.write(line)
+        sys.stdout.flush()
+    else:
+        sys.stdout.flush()
+        os.write(_JSON_FD, line.encode())
 
 
 class ClockSampler:
@@ -335,7 +354,7 @@ def main():
         return run_reference(args)
 
     # (the JSON line is the only stdout output: NCCL's version banner would precede it)
-    os.environ.setdefault("NCCL_DEBUG", "WARN")
+    _stdout_json_only()
     import torch
     import torch.distributed as dist
 
