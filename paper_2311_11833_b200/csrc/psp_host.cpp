@@ -1393,9 +1393,12 @@ static psp_status factor_impl(psp_handle h, const double* A_vals, double pivot_t
   cudaSetDevice(h->device);
   psp_status s;
   const double* tol_dev = nullptr;
+  // (one Jacobian: the default tolerance rides in the program-patch launch below)
+  const bool tol_fused = pivot_tol <= 0 && mj.lanes_per <= 0 && P.f_npatch > 0;
   if (pivot_tol <= 0) {
-    CUDA_TRY(h, psp::launch_pivot_tol(P, A_vals, (double*)h->tol_d.p, h->stream,
-                                      mj.lanes_per > 0 ? h->K / mj.lanes_per : 1));
+    if (!tol_fused)
+      CUDA_TRY(h, psp::launch_pivot_tol(P, A_vals, (double*)h->tol_d.p, h->stream,
+                                        mj.lanes_per > 0 ? h->K / mj.lanes_per : 1));
     tol_dev = (const double*)h->tol_d.p;
   }
   if (!LI.f_pend_smem) {
@@ -1412,8 +1415,12 @@ static psp_status factor_impl(psp_handle h, const double* A_vals, double pivot_t
       if ((s = ensure(h, h->X_d, need))) return s;
     }
   }
-  CUDA_TRY(h, psp::launch_patch_program(P, const_cast<int32_t*>(P.f_stream), A_vals,
-                                        (const double*)h->dperm_d.p, b, h->stream));
+  if (tol_fused)
+    CUDA_TRY(h, psp::launch_patch_tol(P, const_cast<int32_t*>(P.f_stream), A_vals,
+                                      (const double*)h->dperm_d.p, b, (double*)h->tol_d.p, h->stream));
+  else
+    CUDA_TRY(h, psp::launch_patch_program(P, const_cast<int32_t*>(P.f_stream), A_vals,
+                                          (const double*)h->dperm_d.p, b, h->stream));
   if (!LI.f_scr_smem) {
     size_t need = sizeof(double) * (size_t)h->K_pad * 2 * P.c_scr;
     if (h->fscr_d.bytes < need) {

@@ -141,6 +141,8 @@ cudaError_t configure_kernels(const DevicePlan& p, LaunchInfo& li, int force_gro
 // `stream_out` (device copy).
 cudaError_t launch_patch_program(const DevicePlan& p, int32_t* stream_out, const double* A_vals,
                                  const double* dperm, const double* b, cudaStream_t stream);
+cudaError_t launch_patch_tol(const DevicePlan& p, int32_t* stream_out, const double* A_vals,
+                             const double* dperm, const double* b, double* tol_out, cudaStream_t stream);
 cudaError_t launch_pivot_tol(const DevicePlan& p, const double* A_vals, double* tol_out,
                              cudaStream_t stream, int32_t n_jac = 1);
 cudaError_t launch_factor(const DevicePlan& p, const LaunchInfo& li, const int32_t* prog,
