@@ -13,4 +13,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:fact
   -o gpurun_out/f_factor_full -f $CMD > gpurun_out/f_ncu_ff.log 2>&1; echo ncu2=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:solve_kernel_tmem -s 3 -c 1 \
   -o gpurun_out/f_solve_full -f $CMD > gpurun_out/f_ncu_sf.log 2>&1; echo ncu3=$?
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:recover_blk -s 3 -c 1 \
+  -o gpurun_out/f_recover_full -f $CMD > gpurun_out/f_ncu_rf.log 2>&1; echo ncu4=$?
 python tools/gpu/ksweep.py > gpurun_out/f_ksweep.txt 2>&1; echo ksweep=$?
