@@ -173,6 +173,39 @@ def test_uniform_ladder_recover_matches_general_path(L):
     assert rel(np.delete(xu, bad, axis=0), xo) <= 1e-10
 
 
+@pytest.mark.parametrize("L", [2, 4, 8, 16])
+def test_block_recover_small_system(L):
+    """recover_blk_kernel on the 14-bus system (n = 24: every L fits its shared-memory
+    un-permute area, L = 2 included, which the 300-bus test above leaves to the gather
+    kernel), three right-hand sides, a last 32-lane block that is only partly covered by
+    weight rows: bitwise equal to the general path (the same weights made non-uniform by
+    an empty row), within 1e-10 of the oracle's combination (Alg. 1 steps 3-4)."""
+    w = config(0)
+    s = w.system()
+    rng = np.random.default_rng(170 + L)
+    K = 3 * 32 + L
+    eps = rng.choice([-1, 1], K) * 10.0 ** rng.uniform(-4, -2, K)
+    W = K // L
+    wv = rng.normal(size=W * L)
+    wp = np.arange(W + 1, dtype=np.int32) * L
+    wl = np.arange(W * L, dtype=np.int32)
+    B = np.stack([s.b[:, 0], rng.normal(size=s.n), rng.normal(size=s.n)], axis=1)
+    g = gpu_run(s, eps, "mindeg", -1, 0.0, B=B, w_csr=(wp, wl, wv))
+    solver = g["solver"]
+    solver.psp_set_weights(np.r_[wp, wp[-1]].astype(np.int32), wl, wv)
+    xg = solver.psp_recover().cpu().numpy()
+    solver.close()
+    xu = g["xhat"]
+    assert g["rc"] == 0 and (g["status"] == 0).all()
+    assert xu.shape == (W, 3, s.n) and np.array_equal(xu, xg[:W]) and (xg[W] == 0).all()
+    Xo, sto = oracle.SparseOracle(s, g["operm"]).batch(eps, 0.0, B)
+    assert (sto == 0).all() and np.array_equal(g["X"], Xo)
+    Wm = np.zeros((W, K))
+    for r in range(W):
+        Wm[r, r * L:(r + 1) * L] = wv[r * L:(r + 1) * L]
+    assert rel(xu, oracle.combine(Wm, Xo)) <= 1e-10
+
+
 @pytest.mark.parametrize("ci", [0, 1])
 def test_residual_matches_oracle(ci):
     """psp_residual (a7) on the recovered rows, a zero row (-> ||b||) and a NaN
