@@ -210,6 +210,10 @@ struct psp_ctx {
 
   // --- host-API staging ---
   DevBuf stageA_d, stageB_d, stageX_d;
+  DevBuf stageA2_d, stageB2_d;              // (second input staging pair of the async pipeline)
+  cudaStream_t in_stream = nullptr;         // the async pipeline's host -> device copies
+  cudaEvent_t in_ready[2] = {nullptr, nullptr};
+  bool x_ready_set[2] = {false, false};
   // psp_solve_host_async: x-hat staging double buffer, D2H on a copy stream
   DevBuf stageX2_d;
   cudaStream_t copy_stream = nullptr;
@@ -372,6 +376,18 @@ psp_status psp_destroy(psp_handle h) {
   h->flag_d.release();
   h->stageA_d.release();
   h->stageB_d.release();
+  h->stageA2_d.release();
+  h->stageB2_d.release();
+  if (h->in_stream) {
+    cudaStreamSynchronize(h->in_stream);
+    cudaStreamDestroy(h->in_stream);
+    h->in_stream = nullptr;
+  }
+  for (int q = 0; q < 2; ++q) {
+    if (h->in_ready[q]) cudaEventDestroy(h->in_ready[q]);
+    h->in_ready[q] = nullptr;
+    h->x_ready_set[q] = false;
+  }
   h->stageX_d.release();
   h->stageX2_d.release();
   if (h->copy_stream) {
@@ -500,38 +516,49 @@ psp_status psp_solve_host_async(psp_handle h, const double* A_vals_h, int32_t R,
   psp_status s;
   if (!h->copy_stream) {
     CUDA_TRY(h, cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+    CUDA_TRY(h, cudaStreamCreateWithFlags(&h->in_stream, cudaStreamNonBlocking));
     for (int q = 0; q < 2; ++q) {
       CUDA_TRY(h, cudaEventCreateWithFlags(&h->x_ready[q], cudaEventDisableTiming));
+      CUDA_TRY(h, cudaEventCreateWithFlags(&h->in_ready[q], cudaEventDisableTiming));
       CUDA_TRY(h, cudaEventCreateWithFlags(&h->x_copied[q], cudaEventDisableTiming));
     }
   }
   const int q = h->pipe;
   DevBuf& xs = q ? h->stageX2_d : h->stageX_d;
   const size_t xbytes = sizeof(double) * (size_t)h->W * R * h->n;
-  if (xs.bytes < xbytes || h->stageA_d.bytes < sizeof(double) * h->nnz_A ||
-      h->stageB_d.bytes < sizeof(double) * (size_t)h->n * R) {
+  DevBuf& sa = q ? h->stageA2_d : h->stageA_d;
+  DevBuf& sb = q ? h->stageB2_d : h->stageB_d;
+  if (xs.bytes < xbytes || sa.bytes < sizeof(double) * h->nnz_A ||
+      sb.bytes < sizeof(double) * (size_t)h->n * R) {
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     CUDA_TRY(h, cudaStreamSynchronize(h->copy_stream));
-    if ((s = ensure(h, h->stageA_d, sizeof(double) * h->nnz_A))) return s;
-    if ((s = ensure(h, h->stageB_d, sizeof(double) * (size_t)h->n * R))) return s;
+    CUDA_TRY(h, cudaStreamSynchronize(h->in_stream));
+    if ((s = ensure(h, sa, sizeof(double) * h->nnz_A))) return s;
+    if ((s = ensure(h, sb, sizeof(double) * (size_t)h->n * R))) return s;
     if ((s = ensure(h, xs, xbytes))) return s;
   }
   // the buffer's previous copy to the host must be done before recover overwrites it
   if (h->x_copied_set[q]) CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->x_copied[q], 0));
-  CUDA_TRY(h, cudaMemcpyAsync(h->stageA_d.p, A_vals_h, sizeof(double) * h->nnz_A,
-                              cudaMemcpyHostToDevice, h->stream));
-  CUDA_TRY(h, cudaMemcpyAsync(h->stageB_d.p, B_h, sizeof(double) * (size_t)h->n * R,
-                              cudaMemcpyHostToDevice, h->stream));
+  // the inputs travel on their own stream into this step's staging pair, so that their
+  // copies overlap the previous call's kernels; the pair was last read by the call two
+  // steps back (everything up to its x_ready event)
+  if (h->x_ready_set[q]) CUDA_TRY(h, cudaStreamWaitEvent(h->in_stream, h->x_ready[q], 0));
+  CUDA_TRY(h, cudaMemcpyAsync(sa.p, A_vals_h, sizeof(double) * h->nnz_A, cudaMemcpyHostToDevice,
+                              h->in_stream));
+  CUDA_TRY(h, cudaMemcpyAsync(sb.p, B_h, sizeof(double) * (size_t)h->n * R, cudaMemcpyHostToDevice,
+                              h->in_stream));
+  CUDA_TRY(h, cudaEventRecord(h->in_ready[q], h->in_stream));
+  CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->in_ready[q], 0));
   if (R == 1) {
-    if ((s = psp_factor_solve_batch(h, (const double*)h->stageA_d.p, (const double*)h->stageB_d.p,
-                                    pivot_tol, nullptr)))
+    if ((s = psp_factor_solve_batch(h, (const double*)sa.p, (const double*)sb.p, pivot_tol, nullptr)))
       return s;
   } else {
-    if ((s = psp_factor_batch(h, (const double*)h->stageA_d.p, pivot_tol, nullptr))) return s;
-    if ((s = psp_solve_batch(h, R, (const double*)h->stageB_d.p, h->n))) return s;
+    if ((s = psp_factor_batch(h, (const double*)sa.p, pivot_tol, nullptr))) return s;
+    if ((s = psp_solve_batch(h, R, (const double*)sb.p, h->n))) return s;
   }
   if ((s = psp_recover(h, (double*)xs.p))) return s;
   CUDA_TRY(h, cudaEventRecord(h->x_ready[q], h->stream));
+  h->x_ready_set[q] = true;
   CUDA_TRY(h, cudaStreamWaitEvent(h->copy_stream, h->x_ready[q], 0));
   CUDA_TRY(h, cudaMemcpyAsync(x_h, xs.p, xbytes, cudaMemcpyDeviceToHost, h->copy_stream));
   CUDA_TRY(h, cudaEventRecord(h->x_copied[q], h->copy_stream));
