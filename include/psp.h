@@ -436,9 +436,11 @@ psp_status psp_solve_host(psp_handle h, const double* A_vals_h, int32_t R, const
                           double pivot_tol, double* x_h);
 
 /* Pipelined form of psp_solve_host for a stream of systems: enqueues the same work
- * (copies up, factor + solve + recover, x_h copied back on a second, library-owned
- * stream from a double-buffered device staging area) and returns without waiting, so
- * the copy back of one call overlaps the next call's kernels.  A_vals_h, B_h and x_h
+ * (A_vals_h and B_h copied up on a library-owned input stream into a double-buffered
+ * staging pair, factor + solve + recover on the handle's stream, x_h copied back on a
+ * second library-owned stream from a double-buffered device staging area) and returns
+ * without waiting, so the copies of one call overlap the kernels of its neighbours.
+ * A_vals_h, B_h and x_h
  * must be pinned and stay valid (x_h unread) until psp_synchronize; lane statuses via
  * psp_get_lane_status afterwards.  Errors: ARG, STATE, ALLOC, CUDA. */
 psp_status psp_solve_host_async(psp_handle h, const double* A_vals_h, int32_t R, const double* B_h,
